@@ -1,0 +1,370 @@
+"""Seeded synthetic inputs shared by the CUDA path's tests/bench and the oracle.
+
+This module holds NO arithmetic of the method (no cylinders, planes, subdivision or
+traversal).  It only draws curves and rays: generic Bezier evaluation for placing targets,
+the five cubic constraints as a rejection filter, and a sampled thick-fiber
+check standing in for the quartic test of P:673-697.  Recipes: DESIGN.md "Inputs" and
+SURVEY.md 8(d).  Everything is drawn in FP64 with numpy PCG64 and rounded ONCE to FP32;
+the FP32 arrays are canonical (both sides read exactly those).
+
+Array formats (also the C-ABI formats, include/fiber.h):
+  rays   f32[n_rays, 8]   (ox, oy, oz, tmax, dx, dy, dz, 0)    |d| = 1 (rounded)
+  ctrl   f32[n_segs, 4, 3] control point positions
+  radii  f32[n_segs, 4]    radius at each control point
+  pairs  u32[n_pairs, 2]   (ray index, segment index)
+"""
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# The three single fibers of config C1/C2: figure curves of PAPER.md,
+# normalised to unit chord and lifted to 3-D with a small z.
+#   F_A from fig:representation P:399-402; F_B from Fig:EvilConfiguration P:653-656;
+#   F_C from the App. B cubic figure P:1069-1072.
+FIBER_A = np.array([[0, 0, 0], [.25, .375, .08], [.5, .25, -.04], [1, 0, 0]], dtype=np.float64)
+FIBER_B = np.array([[0, 0, 0], [1 / 3, 1 / 6, .05], [2 / 3, 1 / 6, .05], [1, 0, 0]],
+                   dtype=np.float64)
+FIBER_C = np.array([[0, 0, 0], [1 / 3, 7 / 18, .1], [2 / 3, 7 / 18, -.1], [1, 0, 0]],
+                   dtype=np.float64)
+FIBERS = {"A": FIBER_A, "B": FIBER_B, "C": FIBER_C}
+
+
+@dataclass
+class Workload:
+    name: str
+    rays: np.ndarray
+    ctrl: np.ndarray
+    radii: np.ndarray
+    pairs: np.ndarray
+    depth: int
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_pairs(self) -> int:
+        return int(self.pairs.shape[0])
+
+    def sha256(self) -> str:
+        h = hashlib.sha256()
+        for a in (self.rays, self.ctrl, self.radii, self.pairs):
+            h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()
+
+    def subsample(self, n: int, seed: int = 12345) -> "Workload":
+        """Seeded subsample of n pairs (same rays/segments arrays)."""
+        if n >= self.n_pairs:
+            return self
+        idx = np.sort(np.random.Generator(np.random.PCG64(seed)).choice(self.n_pairs, n,
+                                                                         replace=False))
+        return Workload(self.name + f"[sub{n}]", self.rays, self.ctrl, self.radii,
+                        np.ascontiguousarray(self.pairs[idx]), self.depth,
+                        dict(self.meta, subsample_of=self.n_pairs, subsample_seed=seed))
+
+
+# ---------------------------------------------------------------------------------------
+# generic helpers (no method arithmetic)
+# ---------------------------------------------------------------------------------------
+def _rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def _unit(v: np.ndarray) -> np.ndarray:
+    return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+
+def _sphere(rng, n) -> np.ndarray:
+    return _unit(rng.normal(size=(n, 3)))
+
+
+def bezier(P: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """Point of cubic Bezier(s) P[..., 4, k] at u (broadcast over leading dims)."""
+    u = np.asarray(u, dtype=np.float64)[..., None]
+    v = 1.0 - u
+    return (v ** 3 * P[..., 0, :] + 3 * u * v * v * P[..., 1, :] + 3 * u * u * v * P[..., 2, :]
+            + u ** 3 * P[..., 3, :])
+
+
+def bezier_tangent(P: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """Derivative of cubic Bezier(s) at u."""
+    u = np.asarray(u, dtype=np.float64)[..., None]
+    v = 1.0 - u
+    return 3 * (v * v * (P[..., 1, :] - P[..., 0, :]) + 2 * u * v * (P[..., 2, :] - P[..., 1, :])
+                + u * u * (P[..., 3, :] - P[..., 2, :]))
+
+
+def constraint_margins(P: np.ndarray) -> np.ndarray:
+    """The five inner products of P:616-620 (all >= 0 for a valid cubic), shape [..., 5]."""
+    p0, p1, p2, p3 = P[..., 0, :3], P[..., 1, :3], P[..., 2, :3], P[..., 3, :3]
+
+    def d(a, b):
+        return np.sum(a * b, axis=-1)
+
+    return np.stack([d(p2 - p0, p1 - p0), d(p3 - p1, p1 - p0), d(p3 - p1, p3 - p2),
+                     d(p2 - p0, p3 - p2), d(p2 - p0, p3 - p1)], axis=-1)
+
+
+def thick_ok(P: np.ndarray, rbar: np.ndarray, samples: int = 256) -> np.ndarray:
+    """Sampled stand-in for the thick-fiber test: no point of the normal disc of
+    radius rbar at any sampled u reaches beyond the segment's end planes."""
+    u = np.linspace(0.0, 1.0, samples)
+    X = bezier(P[:, None, :, :3], u[None, :])             # [n, s, 3]
+    T = _unit(bezier_tangent(P[:, None, :, :3], u[None, :]))
+    ok = np.ones(P.shape[0], dtype=bool)
+    for end, idx in ((0, (0, 1)), (1, (3, 2))):
+        q = P[:, idx[0], :3]
+        n = _unit(P[:, idx[0], :3] - P[:, idx[1], :3])      # outward normal of the end plane
+        # furthest extent of the disc (centre X, normal T, radius r) along n:
+        #   <X - q, n> + r * sqrt(1 - <T, n>^2)
+        tn = np.sum(T * n[:, None, :], axis=-1)
+        ext = np.sum((X - q[:, None, :]) * n[:, None, :], axis=-1) + rbar[:, None] * np.sqrt(
+            np.clip(1 - tn * tn, 0, None))
+        # exclude the end sample itself (its disc lies in the plane by construction)
+        sl = slice(1, None) if end == 0 else slice(0, -1)
+        ok &= np.all(ext[:, sl] <= 1e-12, axis=1)
+    return ok
+
+
+def _pack_rays(orig: np.ndarray, dirs: np.ndarray, tmax=np.inf) -> np.ndarray:
+    n = orig.shape[0]
+    r = np.zeros((n, 8), dtype=np.float32)
+    r[:, 0:3] = orig
+    r[:, 3] = tmax
+    r[:, 4:7] = _unit(dirs)
+    return r
+
+
+# ---------------------------------------------------------------------------------------
+# C1 / C2: one fiber
+# ---------------------------------------------------------------------------------------
+def single_fiber(name: str = "A", radius: float = 0.01):
+    P = FIBERS[name]
+    ctrl = P[None].astype(np.float32)
+    radii = np.full((1, 4), radius, dtype=np.float32)
+    return ctrl, radii
+
+
+def _curve_samples(ctrl: np.ndarray, n: int = 1025) -> np.ndarray:
+    return bezier(ctrl[0].astype(np.float64), np.linspace(0, 1, n))
+
+
+def config1(depth: int = 4, fiber: str = "A", seed: int = 0) -> Workload:
+    """C1: 64x64 orthographic rays, direction normalize(0.3, -0.2, 1), over the fiber's
+    projected AABB dilated by r, origins 3 units back, D = 4."""
+    ctrl, radii = single_fiber(fiber)
+    r = float(radii.max())
+    w = _unit(np.array([0.3, -0.2, 1.0]))
+    e1 = _unit(np.cross(w, [0.0, 1.0, 0.0]))
+    e2 = np.cross(w, e1)
+    X = _curve_samples(ctrl)
+    m = 0.5 * (X.min(0) + X.max(0))
+    a = (X - m) @ e1
+    b = (X - m) @ e2
+    ga = np.linspace(a.min() - r, a.max() + r, 64)
+    gb = np.linspace(b.min() - r, b.max() + r, 64)
+    A, B = np.meshgrid(ga, gb, indexing="ij")
+    orig = m + A.reshape(-1, 1) * e1 + B.reshape(-1, 1) * e2 - 3.0 * w
+    rays = _pack_rays(orig, np.broadcast_to(w, orig.shape))
+    pairs = np.stack([np.arange(4096), np.zeros(4096)], 1).astype(np.uint32)
+    return Workload(f"C1:fiber{fiber}:ortho64x64", rays, ctrl, radii, pairs, depth,
+                    {"seed": seed, "fiber": fiber})
+
+
+def config2(fiber: str = "A", n_rays: int = 1 << 20, depth: int = 22, seed: int | None = None,
+            targeted: bool = False) -> Workload:
+    """C2: 2^20 random rays against one fiber.  Origins uniform on a sphere of radius 2 about
+    the AABB centre; targets uniform in the AABB dilated by r (or, 'targeted', within 2r of
+    the curve).  Seeds 1, 2, 3 for fibers A, B, C."""
+    if seed is None:
+        seed = {"A": 1, "B": 2, "C": 3}[fiber]
+    rng = _rng(seed)
+    ctrl, radii = single_fiber(fiber)
+    r = float(radii.max())
+    X = _curve_samples(ctrl)
+    lo, hi = X.min(0) - r, X.max(0) + r
+    c = 0.5 * (lo + hi)
+    orig = c + 2.0 * _sphere(rng, n_rays)
+    if targeted:
+        u = rng.uniform(0, 1, n_rays)
+        tgt = bezier(ctrl[0].astype(np.float64), u) + 2 * r * rng.uniform(-1, 1, (n_rays, 3))
+    else:
+        tgt = lo + (hi - lo) * rng.uniform(0, 1, (n_rays, 3))
+    rays = _pack_rays(orig, tgt - orig)
+    pairs = np.stack([np.arange(n_rays), np.zeros(n_rays)], 1).astype(np.uint32)
+    return Workload(f"C2:fiber{fiber}:{'targeted' if targeted else 'random'}{n_rays}", rays, ctrl,
+                    radii, pairs, depth, {"seed": seed, "fiber": fiber})
+
+
+# ---------------------------------------------------------------------------------------
+# hair / fur geometry (C3, C4, C5)
+# ---------------------------------------------------------------------------------------
+def _catmull_rom_segments(pts: np.ndarray) -> np.ndarray:
+    """pts [S, K+1, 3] polyline -> Bezier control points [S, K, 4, 3] (uniform Catmull-Rom)."""
+    ext = np.concatenate([2 * pts[:, :1] - pts[:, 1:2], pts, 2 * pts[:, -1:] - pts[:, -2:-1]], 1)
+    p_prev, p0, p1, p_next = ext[:, :-3], ext[:, 1:-2], ext[:, 2:-1], ext[:, 3:]
+    b1 = p0 + (p1 - p_prev) / 6.0
+    b2 = p1 - (p_next - p0) / 6.0
+    return np.stack([p0, b1, b2, p1], axis=2)
+
+
+def _random_walk(rng, roots, start_dir, n_steps, step, max_turn_deg):
+    """Strand polylines: each step turns the direction by <= max_turn_deg."""
+    S = roots.shape[0]
+    pts = np.zeros((S, n_steps + 1, 3))
+    pts[:, 0] = roots
+    d = _unit(start_dir)
+    for k in range(n_steps):
+        # rotate d by an angle in [0, max_turn] about a random axis perpendicular to d
+        ax = _unit(np.cross(d, rng.normal(size=(S, 3))))
+        ang = np.deg2rad(max_turn_deg) * rng.uniform(0, 1, S)[:, None]
+        d = _unit(d * np.cos(ang) + np.cross(ax, d) * np.sin(ang))
+        pts[:, k + 1] = pts[:, k] + step * d
+    return pts
+
+
+def hair_patch(seed: int = 3374, n_side: int = 100, n_seg: int = 10, thin: bool = False):
+    """10,000 strands x 10 C1 cubic segments over the unit xz-square."""
+    rng = _rng(seed)
+    g = (np.arange(n_side) + 0.5) / n_side
+    gx, gz = np.meshgrid(g, g, indexing="ij")
+    roots = np.stack([gx.ravel(), np.zeros(gx.size), gz.ravel()], 1)
+    roots[:, [0, 2]] += rng.uniform(-0.4, 0.4, (roots.shape[0], 2)) / n_side
+    S = roots.shape[0]
+    pts = _random_walk(rng, roots, np.tile([0.0, 1.0, 0.0], (S, 1)), n_seg, 0.1, 25.0)
+    segs = _catmull_rom_segments(pts).reshape(-1, 4, 3)
+    chord = np.linalg.norm(segs[:, 3] - segs[:, 0], axis=1)
+    if thin:
+        radii = np.repeat((1e-4 * chord)[:, None], 4, 1)
+    else:
+        # taper 4e-3 -> 1e-3 along each strand, cubic radius per control point
+        k = np.tile(np.arange(n_seg), S).astype(np.float64)
+        s = (k[:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None]) / n_seg
+        radii = 4e-3 + (1e-3 - 4e-3) * s
+    return _validate(segs, radii)
+
+
+def fur_ball(seed: int = 3376, n_strands: int = 524288, n_seg: int = 4):
+    """Fur: strands on the unit sphere, length 0.2, outward, curl <= 20 deg per segment."""
+    rng = _rng(seed)
+    roots = _sphere(rng, n_strands)
+    pts = _random_walk(rng, roots, roots.copy(), n_seg, 0.2 / n_seg, 20.0)
+    segs = _catmull_rom_segments(pts).reshape(-1, 4, 3)
+    k = np.tile(np.arange(n_seg), n_strands).astype(np.float64)
+    s = (k[:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None]) / n_seg
+    radii = 1.5e-3 + (4e-4 - 1.5e-3) * s
+    return _validate(segs, radii)
+
+
+def _validate(segs: np.ndarray, radii: np.ndarray):
+    """Enforce the preconditions of the path on every segment (SURVEY 8(d) "Inputs"):
+    the five constraints, |t0|, |t1| >= 0.05 |d|, and the sampled thick-fiber check.
+    A violating segment is straightened towards its chord until valid."""
+    segs = segs.copy()
+    for it in range(8):
+        m = constraint_margins(segs)
+        d = np.linalg.norm(segs[:, 3] - segs[:, 0], axis=1)
+        t0 = np.linalg.norm(segs[:, 1] - segs[:, 0], axis=1)
+        t1 = np.linalg.norm(segs[:, 3] - segs[:, 2], axis=1)
+        ok = (m.min(1) >= 1e-3 * d * d) & (t0 >= 0.05 * d) & (t1 >= 0.05 * d)
+        ok &= thick_ok(segs, radii.max(1))
+        if ok.all():
+            break
+        bad = ~ok
+        lin = segs[bad, 0][:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None, :, None] * (
+            segs[bad, 3] - segs[bad, 0])[:, None]
+        segs[bad] = 0.5 * segs[bad] + 0.5 * lin
+    return segs.astype(np.float32), radii.astype(np.float32)
+
+
+def _targets_on_segments(rng, ctrl, radii, seg_idx, dirs, scale_lo, scale_hi):
+    """Target points at distance rho = r(u) * (1 + xi) from C(u), along n = w x C'(u)."""
+    P = ctrl[seg_idx].astype(np.float64)
+    u = rng.uniform(0.02, 0.98, seg_idx.shape[0])
+    C = bezier(P, u)
+    T = bezier_tangent(P, u)
+    rr = bezier(radii[seg_idx].astype(np.float64)[..., None], u)[:, 0]
+    n = _unit(np.cross(dirs, T))
+    xi = rng.uniform(scale_lo, scale_hi, seg_idx.shape[0])
+    return C + (rr * (1 + xi))[:, None] * n
+
+
+def config3(seed: int = 3374, n_rays: int = 1 << 20, k: int = 16, depth: int = 9) -> Workload:
+    """C3: hair patch, 2^20 targeted rays x (target segment + 15 nearest) = 2^24 pairs, D=9."""
+    from scipy.spatial import cKDTree
+
+    ctrl, radii = hair_patch(seed)
+    rng = _rng(seed + 1)
+    seg = rng.integers(0, ctrl.shape[0], n_rays)
+    w = _sphere(rng, n_rays)
+    tgt = _targets_on_segments(rng, ctrl, radii, seg, w, -1.5, 0.5)
+    orig = tgt - 2.0 * w
+    rays = _pack_rays(orig, w)
+    centers = 0.5 * (ctrl.min(1) + ctrl.max(1)).astype(np.float64)
+    _, nn = cKDTree(centers).query(tgt, k=k)
+    nn = np.asarray(nn)
+    # make sure the target segment is among the candidates (replace the k-th if absent)
+    has = (nn == seg[:, None]).any(1)
+    nn[~has, -1] = seg[~has]
+    pairs = np.stack([np.repeat(np.arange(n_rays), k), nn.ravel()], 1).astype(np.uint32)
+    order = np.lexsort((pairs[:, 0], pairs[:, 1]))
+    pairs = np.ascontiguousarray(pairs[order])
+    return Workload("C3:hair100k:16M", rays, ctrl, radii, pairs, depth, {"seed": seed})
+
+
+def config4(seed: int = 3375, n_rays: int = 1 << 24, depth: int = 22) -> Workload:
+    """C4: thin fibers (r = 1e-4 chord), one pair per ray, half grazing (xi in +-2e-3),
+    half inside (xi in [-1, 0]); D = 22."""
+    ctrl, radii = hair_patch(seed - 1, thin=True)
+    rng = _rng(seed)
+    seg = rng.integers(0, ctrl.shape[0], n_rays)
+    w = _sphere(rng, n_rays)
+    half = n_rays // 2
+    tgt = np.concatenate([
+        _targets_on_segments(rng, ctrl, radii, seg[:half], w[:half], -2e-3, 2e-3),
+        _targets_on_segments(rng, ctrl, radii, seg[half:], w[half:], -1.0, 0.0)])
+    orig = tgt - 2.0 * w
+    rays = _pack_rays(orig, w)
+    pairs = np.stack([np.arange(n_rays), seg], 1).astype(np.uint32)
+    return Workload(f"C4:thin:{n_rays}", rays, ctrl, radii, pairs, depth, {"seed": seed})
+
+
+def config5(seed: int = 3376, n_rays: int = 1 << 24, k: int = 16, depth: int = 6,
+            n_strands: int = 524288, ray_range: tuple[int, int] | None = None) -> Workload:
+    """C5: fur, 2^21 segments, 2^24 targeted rays x 16 candidates = 2^28 pairs, D = 6.
+    ray_range=(a, b) generates only the pairs of rays a..b-1 (per-rank shard) -- the rays,
+    segments and candidate choice are identical to the full generation."""
+    from scipy.spatial import cKDTree
+
+    ctrl, radii = fur_ball(seed, n_strands)
+    rng = _rng(seed + 1)
+    seg = rng.integers(0, ctrl.shape[0], n_rays)
+    w = _sphere(rng, n_rays)
+    tgt = _targets_on_segments(rng, ctrl, radii, seg, w, -1.5, 0.5)
+    orig = tgt - 0.5 * w
+    rays = _pack_rays(orig, w)
+    a, b = ray_range if ray_range is not None else (0, n_rays)
+    centers = 0.5 * (ctrl.min(1) + ctrl.max(1)).astype(np.float64)
+    _, nn = cKDTree(centers).query(tgt[a:b], k=k, workers=-1)
+    nn = np.asarray(nn)
+    has = (nn == seg[a:b, None]).any(1)
+    nn[~has, -1] = seg[a:b][~has]
+    pairs = np.stack([np.repeat(np.arange(a, b), k), nn.ravel()], 1).astype(np.uint32)
+    order = np.lexsort((pairs[:, 0], pairs[:, 1]))
+    return Workload(f"C5:fur2M:rays[{a},{b})", rays, ctrl, radii,
+                    np.ascontiguousarray(pairs[order]), depth, {"seed": seed})
+
+
+def straight_fiber(length: float = 6.0, r0: float = 0.1, r3: float | None = None,
+                   axis=(1.0, 0.0, 0.0), origin=(0.0, 0.0, 0.0)):
+    """Straight fiber with evenly spaced control points (exact finite cylinder / taper)."""
+    r3 = r0 if r3 is None else r3
+    a = np.asarray(axis, dtype=np.float64)
+    o = np.asarray(origin, dtype=np.float64)
+    ctrl = np.stack([o + (i / 3.0) * length * a for i in range(4)])[None].astype(np.float32)
+    radii = np.array([[r0 + (r3 - r0) * i / 3.0 for i in range(4)]], dtype=np.float32)
+    return ctrl, radii
+
+
+def make_pairs_1seg(n_rays: int) -> np.ndarray:
+    return np.stack([np.arange(n_rays), np.zeros(n_rays)], 1).astype(np.uint32)
