@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the ray/fiber hot path (BASELINE.json metric: G ray-fiber tests/s vs
+subdivision depth 2-22, % of the FP32 roofline).
+
+Workload (N = 1): config C2 -- each of the three single fibers F_A, F_B, F_C against 2^20
+random rays, at every depth D = 2..22 (Fig. 1).  One step = the whole
+sweep: 3 fibers x 21 depths = 63 launches of fiber_intersect, 66,060,288 ray-segment tests.
+With N > 1 ranks (torchrun), every rank runs the same sweep on its own rays (weak scaling:
+rays are sharded, segments replicated); after the timed region the
+per-ray hit records are gathered with one NCCL all_gather.
+
+Timing: W untimed warm-up steps, then K steps.  Every launch is bracketed by CUDA events on
+its stream and preceded (untimed) by a 256 MiB write that flushes the 126 MB L2, so every
+launch reads its rays/pairs from HBM.  value = all ranks' tests / max over ranks of the
+summed kernel time.  `--impl reference` times the FP64 CPU oracle instead (bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "G ray-fiber tests/s vs subdivision depth (2-22), % FP32 roofline"
+UNIT = "G ray-fiber tests/s"
+FIBERS = ("A", "B", "C")
+DEPTHS = tuple(range(2, 23))
+N_RAYS = 1 << 20
+
+# Algorithmic FP32 flops per occurrence of each step of the loop (FMA = 2), counted from
+# the kernel source: a3 node test, a4 descend, a5 backtrack.
+FLOPS_TEST, FLOPS_DESCEND, FLOPS_BACKTRACK = 64, 49, 170
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--rays", type=int, default=N_RAYS)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------- workload
+def make_workloads(rank: int, n_rays: int):
+    from workloads import gen
+
+    # rank r draws its own rays (weak scaling); rank 0 reproduces the single-GPU seeds
+    return [gen.config2(f, n_rays=n_rays, depth=22, seed={"A": 1, "B": 2, "C": 3}[f] + 1000 * rank)
+            for f in FIBERS]
+
+
+def algorithmic_flops(g) -> float:
+    tests = g["tests"].astype(np.float64)
+    bt = g["backtracks"].astype(np.float64)
+    desc = np.maximum(tests - bt - 1, 0)
+    return float((FLOPS_TEST * tests + FLOPS_DESCEND * desc + FLOPS_BACKTRACK * bt).sum())
+
+
+def fp32_peak_tflops(sms: int, mhz: float) -> float:
+    return sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_03374_b200 as fx
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    fx.lib()
+    wls = make_workloads(rank, args.rays)
+    data = [fx.to_device(w, dev) for w in wls]
+    n = args.rays
+    hits = torch.empty((n, 4), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = [(fi, D) for fi in range(len(FIBERS)) for D in DEPTHS]
+    pairs_per_step = n * len(launches)
+
+    def step(record):
+        ms = []
+        for fi, D in launches:
+            rays, segs, pairs = data[fi]
+            flush.fill_(1)  # untimed L2 flush: inputs come from HBM
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            fx.intersect(rays, segs, pairs, D, hits=hits)
+            if record:
+                e1.record(stream)
+                ms.append((e0, e1))
+        return ms
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        evs = [step(True) for _ in range(args.steps)]
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    per_launch = np.array([[a.elapsed_time(b) for a, b in s] for s in evs])  # [K, 63] ms
+    total_ms = float(per_launch.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * pairs_per_step * args.steps / (total_ms * 1e-3) / 1e9
+
+    # per-launch counters (deterministic) for the algorithmic flop count, by depth
+    flops = np.zeros(len(launches))
+    hitfrac = np.zeros(len(launches))
+    for j, (fi, D) in enumerate(launches):
+        rays, segs, pairs = data[fi]
+        g = fx.unpack(fx.intersect(rays, segs, pairs, D))
+        flops[j] = algorithmic_flops(g)
+        hitfrac[j] = g["hit"].mean()
+    mean_ms = per_launch.mean(0)  # per launch, over steps
+    by_depth = {}
+    for D in DEPTHS:
+        idx = [j for j, (fi, d) in enumerate(launches) if d == D]
+        by_depth[str(D)] = round(n * len(idx) / (mean_ms[idx].sum() * 1e-3) / 1e9, 3)
+    clocks = clk.summary()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_mhz = clocks["sm_max_mhz"] or 1965.0
+    peak = fp32_peak_tflops(sms, peak_mhz)
+    achieved = float(flops.sum() / (mean_ms.sum() * 1e-3) / 1e12)
+
+    # gather per-ray hit records across ranks (the one collective)
+    gather_ms = None
+    if world > 1:
+        from paper_1811_03374_b200 import dist as fxd
+
+        gather_ms = fxd.timed_gather(hits)
+
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded; workloads/gen.py config2)",
+        "config": {"workload": "C2: single cubic fiber x 2^20 random rays, fibers F_A/F_B/F_C, "
+                               "depth sweep 2-22 (Fig. 1 shape)",
+                   "rays_per_fiber_per_rank": n, "depths": [DEPTHS[0], DEPTHS[-1]],
+                   "launches_per_step": len(launches), "tests_per_step_per_rank": pairs_per_step,
+                   "l2": "flushed (256 MiB write) before every timed launch",
+                   "parallelism": f"ray-sharded x{world}"},
+        "by_depth": by_depth,
+        "drop_4_22": round(by_depth["4"] / by_depth["22"], 3),
+        "hit_fraction_by_depth": {str(D): round(float(np.mean(
+            [hitfrac[j] for j, (fi, d) in enumerate(launches) if d == D])), 4) for D in DEPTHS},
+        "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_basis": f"FP32: {sms} SMs x 128 lanes x 2 x {peak_mhz:.0f} MHz "
+                                   "(max SM clock; B200_PROFILING.md unit counts)",
+                     "kernel": "intersect_kernel (K2)"},
+        "gpu_launches": args.steps * len(launches),
+        "clocks": clocks,
+        "wall_s_timed": round(wall, 3),
+    }
+    if gather_ms is not None:
+        out["gather_ms"] = gather_ms
+    if not args.no_e2e:
+        out["e2e"] = e2e(args, fx, wls, dev)
+    if rank == 0 and not args.no_cpu and world == 1:
+        out["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(args, fx, wls, dev):
+    """Same metric through the public API with HOST buffers: every step copies each fiber's
+    rays and pairs host->device (pinned) and every launch's hits device->host."""
+    import torch
+
+    n = args.rays
+    host = []
+    for w in wls:
+        host.append((torch.from_numpy(w.rays).pin_memory(),
+                     torch.from_numpy(w.pairs.view(np.int32)).pin_memory(),
+                     torch.from_numpy(w.ctrl).pin_memory(), torch.from_numpy(w.radii).pin_memory()))
+    hits_h = torch.empty((n, 4), dtype=torch.float32).pin_memory()
+    d_rays = torch.empty((n, 8), dtype=torch.float32, device=dev)
+    d_pairs = torch.empty((n, 2), dtype=torch.int32, device=dev)
+    d_ctrl = torch.empty((1, 4, 3), dtype=torch.float32, device=dev)
+    d_rad = torch.empty((1, 4), dtype=torch.float32, device=dev)
+    d_hits = torch.empty((n, 4), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    h2d = d2h = 0
+
+    def step():
+        nonlocal h2d, d2h
+        h2d = d2h = 0
+        for (r, p, c, ra) in host:
+            d_rays.copy_(r, non_blocking=True)
+            d_pairs.copy_(p, non_blocking=True)
+            d_ctrl.copy_(c, non_blocking=True)
+            d_rad.copy_(ra, non_blocking=True)
+            h2d += r.numel() * 4 + p.numel() * 4 + c.numel() * 4 + ra.numel() * 4
+            segs = fx.build_segments(d_ctrl, d_rad)
+            for D in DEPTHS:
+                fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits)
+                hits_h.copy_(d_hits, non_blocking=True)
+                d2h += d_hits.numel() * 4
+        return h2d, d2h
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, 3))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    tests = n * len(FIBERS) * len(DEPTHS) * k
+    return {"value": round(tests / (ms * 1e-3) / 1e9, 4), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(ms / k, 3), "steps": k}
+
+
+# ------------------------------------------------------------------------------- oracle
+def _oracle_sample(n_per: int, seed_shift: int = 0):
+    from workloads import gen
+
+    ws = []
+    for f in FIBERS:
+        w = gen.config2(f, n_rays=N_RAYS, depth=22)
+        ws.append(w.subsample(n_per, seed=77 + seed_shift))
+    return ws
+
+
+def _time_oracle(ws, nthreads):
+    import oracle
+
+    t0 = time.perf_counter()
+    n = 0
+    for w in ws:
+        for D in DEPTHS:
+            oracle.intersect(w.rays, w.ctrl, w.radii, w.pairs, D, with_eps=False,
+                             nthreads=nthreads)
+            n += w.n_pairs
+    return n, time.perf_counter() - t0
+
+
+def cpu_baseline(n_per: int = 1 << 14):
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    ws = _oracle_sample(n_per)
+    n, el = _time_oracle(ws, cores)
+    return {"value": n / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"C2 subsample: {n_per} of 2^20 rays per fiber x 3 fibers x depths 2-22 "
+                      f"= {n} tests, FP64 oracle without the eps runs, {el:.2f} s wall"}
+
+
+def run_reference(args):
+    """--impl reference: the FP64 CPU oracle as it stands, on a bounded sample per step."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    n_per = 4096
+    ws = _oracle_sample(n_per)
+    for _ in range(args.warmup):
+        _time_oracle(ws[:1], cores)
+    tot_n, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        n, el = _time_oracle(ws, cores)
+        tot_n += n
+        tot_s += el
+    v = tot_n / tot_s / 1e9
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * tot_s / args.steps, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; workloads/gen.py config2)", "impl": "reference",
+           "config": {"workload": "C2: single cubic fiber x random rays, fibers F_A/F_B/F_C, "
+                                  "depth sweep 2-22 (Fig. 1 shape)",
+                      "sample": f"{n_per} rays per fiber per depth per step"},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"{n_per} of 2^20 rays per fiber x 3 fibers x 21 depths "
+                                      "per step"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

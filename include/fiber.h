@@ -1,0 +1,156 @@
+/*
+ * fiber.h -- C ABI of the B200 (sm_100a) ray/fiber intersection library (libfiber.so).
+ *
+ * The operation is the one of Binder & Keller, "Fast, High Precision Ray/Fiber
+ * Intersection using Tight, Disjoint Bounding Volumes" (arXiv 1811.03374): given a ray
+ * (origin, direction, t_max) and a fiber -- a circular contour of cubic-Bezier radius swept
+ * along a cubic Bezier curve -- return the nearest intersection (t, u, normal) or nothing
+ * (lst:algorithm).  The method is the stackless
+ * subdivision with disjoint bounding cylinders at a fixed depth D, with the
+ * readings F1-F9 documented in DESIGN.md.
+ *
+ * Conventions for every call:
+ *   - Pointers marked "device" are CUDA device pointers owned by the caller; the library
+ *     allocates nothing and keeps no global state.  It is re-entrant and thread-safe.
+ *   - Work is enqueued on `cuda_stream` (a cudaStream_t, NULL = legacy default stream) and
+ *     the call returns immediately; outputs are valid after that stream synchronises, and
+ *     inputs must not change before then.  Kernel faults surface at the next sync.
+ *   - Return value: FIBER_OK, or a negative fiber_status.  Argument errors are detected
+ *     before anything is enqueued.  Data errors (NaN, out-of-range indices, segments that
+ *     violate the paper's constraints) never abort: they are reported per record in flags.
+ */
+#ifndef FIBER_H
+#define FIBER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* 23 mantissa bits hold the parametric interval (lst:calculate_interval P:1331-1345,
+ * cur_size = 1 << 23 at P:1605): depth D in [0, 23], min_size = 2^(23 - D). */
+#define FIBER_MAX_DEPTH 23
+
+typedef enum {
+  FIBER_OK = 0,
+  FIBER_EINVAL = -1,  /* NULL pointer with n > 0, n < 0, n >= 2^32, depth not in [0, 23] */
+  FIBER_ECUDA = -2,   /* a CUDA call or launch failed; see fiber_error_string()          */
+  FIBER_EDEVICE = -3  /* the current device is not an sm_100 (B200) GPU                  */
+} fiber_status;
+
+/* A ray o + t d, t in [0, tmax) (unit ray of P:475-481; t_max of P:1610).
+ * d need not be exactly unit: t is the parameter along d as given.  tmax may be +inf. */
+typedef struct {
+  float ox, oy, oz, tmax;
+  float dx, dy, dz, pad;
+} fiber_ray; /* 32 B */
+
+/* One ray-segment candidate (the unit of work; produced by a top-level hierarchy). */
+typedef struct {
+  uint32_t ray, seg;
+} fiber_pair; /* 8 B */
+
+/* Per-pair result (lst:calc_intersection P:1546-1587).
+ *   t      ray parameter of the hit (+inf on a miss)
+ *   u      curve parameter in [0, 1] (0 on a miss)
+ *   n_oct  unit surface normal, octahedral encoding, 2 x snorm16 (x in bits 0-15,
+ *          y in bits 16-31); see fiber_decode_normal().  0 on a miss.
+ *   flags  FIBER_HIT, kind (bits 1-2), FIBER_INSIDE, FIBER_BAD_INPUT, FIBER_BAD_SEGMENT,
+ *          backtracks (bits 8-15, saturating), node tests (bits 16-31, saturating). */
+typedef struct {
+  float t, u;
+  uint32_t n_oct, flags;
+} fiber_hit; /* 16 B */
+
+#define FIBER_HIT (1u << 0)
+#define FIBER_KIND_SHIFT 1
+#define FIBER_KIND_MASK (3u << 1)
+#define FIBER_KIND_LATERAL 0u /* entry through the lateral surface                       */
+#define FIBER_KIND_CAP0 1u    /* entry through the start cap, u = 0 (F6)     */
+#define FIBER_KIND_CAP1 2u    /* entry through the end cap,   u = 1                       */
+#define FIBER_KIND_WEDGE 3u   /* entry through an internal partition plane (low D, F2)   */
+#define FIBER_INSIDE (1u << 3)      /* ray origin inside the fiber: t = 0                   */
+#define FIBER_BAD_INPUT (1u << 4)   /* non-finite ray, zero direction, tmax <= 0, or an index
+                                       out of range: the record is a miss                   */
+#define FIBER_BAD_SEGMENT (1u << 5) /* the segment failed fiber_build_segments' checks; the
+                                       pair is still computed but the result is unspecified
+                                                                                 */
+#define FIBER_BACKTRACKS(f) (((f) >> 8) & 0xffu)
+#define FIBER_NODE_TESTS(f) (((f) >> 16) & 0xffffu)
+
+/* Segment flags written by fiber_build_segments (0 = valid). */
+#define FIBER_SEG_CONSTRAINT(k) (1u << (k)) /* k = 0..4: the k-th cubic inequality of
+                                               P:614-621 fails (App. B eqs)    */
+#define FIBER_SEG_DEGENERATE (1u << 5)      /* zero chord or an end tangent shorter than
+                                               1e-6 of the chord (plane normal undefined)   */
+#define FIBER_SEG_NONFINITE (1u << 6)       /* a NaN/Inf coordinate or radius             */
+#define FIBER_SEG_NEG_RADIUS (1u << 7)      /* a negative radius                           */
+
+/* Device-resident segment set, structure of arrays: p[i][s] = (x, y, z, r) of control
+ * point i of segment s, one float4 plane per control point (16-B aligned, coalesced
+ * float4 loads).  A host-side descriptor of caller-owned device storage. */
+typedef struct {
+  void *p0, *p1, *p2, *p3; /* device float4[n]            */
+  uint32_t *flags;         /* device uint32[n], 0 = valid */
+  int64_t n;
+} fiber_segments;
+
+/* Bytes of device storage needed for n segments (4 float4 planes + flags, 256-B aligned). */
+size_t fiber_segments_bytes(int64_t n);
+
+/* Host-only: carve `storage` (device, >= fiber_segments_bytes(n) bytes, 256-B aligned)
+ * into the SoA planes of `out`.  No device work. */
+int fiber_segments_view(void *storage, int64_t n, fiber_segments *out);
+
+/* Segment preprocessing: pack control points and radii into the SoA
+ * planes of `segs` and validate each segment (the five cubic constraints of P:614-621,
+ * degenerate tangents, non-finite values, negative radii) into segs->flags.
+ *   ctrl_pts  device float[n][4][3]  control point positions (the 4-D control points of
+ *                                    P:485-486 without the radius)
+ *   radii     device float[n][4]     radius at each control point (cubic radius)
+ *   segs      in: a view of n segments (fiber_segments_view); out: filled on device
+ * Errors: FIBER_EINVAL (NULL with n > 0, n < 0, n >= 2^32, segs->n != n),
+ *         FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_build_segments(const float *ctrl_pts, const float *radii, int64_t n,
+                         fiber_segments *segs, void *cuda_stream);
+
+/* The hot path (lst:algorithm): for every pair, intersect rays[pair.ray] with
+ * segment pair.seg at subdivision depth max_depth and write hits[i].
+ *   rays      device fiber_ray[n_rays]
+ *   segs      built by fiber_build_segments (host descriptor, device planes)
+ *   pairs     device fiber_pair[n_pairs]; indices out of range give FIBER_BAD_INPUT
+ *   max_depth D in [0, 23]: the number of halvings of [0, 1]; min_size = 2^(23 - D)
+ *   hits      device fiber_hit[n_pairs]
+ * Results are bit-identical for the same inputs regardless of launch shape or order.
+ * Errors: FIBER_EINVAL, FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_intersect(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
+                    const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
+                    void *cuda_stream);
+
+/* fiber_intersect with the fused per-ray nearest-hit epilogue: in
+ * addition (hits may be NULL), for every hit pair atomically
+ *   nearest[pair.ray] = min(nearest[pair.ray], (bits(t) << 32) | i)
+ * where i is the pair index in this call.  `nearest` (device uint64[n_rays]) must be
+ * initialised by the caller (fiber_nearest_init) before the first call of a batch. */
+int fiber_intersect_nearest(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
+                            const fiber_pair *pairs, int64_t n_pairs, int max_depth,
+                            fiber_hit *hits, uint64_t *nearest, void *cuda_stream);
+
+/* Fill nearest[0..n_rays) with the "no hit" key (all ones). */
+int fiber_nearest_init(uint64_t *nearest, int64_t n_rays, void *cuda_stream);
+
+/* Static description of the last failure on this thread (or of `code`). */
+const char *fiber_error_string(int code);
+
+/* Host helper: decode an octahedral snorm16x2 normal into out[3] (unit length). */
+void fiber_decode_normal(uint32_t n_oct, float out[3]);
+
+/* ABI version (major * 100 + minor). */
+int fiber_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIBER_H */

@@ -1,0 +1,73 @@
+// segments.cu -- K1: segment preprocessing.  One thread per segment: pack
+// (ctrl_pts[n][4][3], radii[n][4]) into four float4 SoA planes (x, y, z, r) and validate
+// the segment against the paper's preconditions (3.4).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "fiber.h"
+#include "fiber_internal.h"
+
+namespace {
+
+__global__ void __launch_bounds__(256) build_segments_kernel(
+    const float* __restrict__ ctrl, const float* __restrict__ radii, int64_t n,
+    float4* __restrict__ p0, float4* __restrict__ p1, float4* __restrict__ p2,
+    float4* __restrict__ p3, uint32_t* __restrict__ flags) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    double P[4][3];
+    float r[4];
+    uint32_t f = 0;
+    for (int i = 0; i < 4; ++i) {
+      r[i] = radii[4 * s + i];
+      for (int k = 0; k < 3; ++k) {
+        float v = ctrl[12 * s + 3 * i + k];
+        if (!isfinite(v)) f |= FIBER_SEG_NONFINITE;
+        P[i][k] = v;
+      }
+      if (!isfinite(r[i])) f |= FIBER_SEG_NONFINITE;
+      if (r[i] < 0.0f) f |= FIBER_SEG_NEG_RADIUS;
+    }
+    auto dotd = [&](int a, int b, int c, int d) {  // <P_a - P_b, P_c - P_d>
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += (P[a][k] - P[b][k]) * (P[c][k] - P[d][k]);
+      return acc;
+    };
+    // the five inequalities of P:616-620 (App. B eqs)
+    if (dotd(2, 0, 1, 0) < 0.0) f |= FIBER_SEG_CONSTRAINT(0);
+    if (dotd(3, 1, 1, 0) < 0.0) f |= FIBER_SEG_CONSTRAINT(1);
+    if (dotd(3, 1, 3, 2) < 0.0) f |= FIBER_SEG_CONSTRAINT(2);
+    if (dotd(2, 0, 3, 2) < 0.0) f |= FIBER_SEG_CONSTRAINT(3);
+    if (dotd(2, 0, 3, 1) < 0.0) f |= FIBER_SEG_CONSTRAINT(4);
+    // degenerate chord or end tangent: the cropping plane normal is undefined
+    double dd = dotd(3, 0, 3, 0), a0 = dotd(1, 0, 1, 0), a1 = dotd(3, 2, 3, 2);
+    if (!(dd > 0.0) || a0 <= 1e-12 * dd || a1 <= 1e-12 * dd) f |= FIBER_SEG_DEGENERATE;
+    p0[s] = make_float4((float)P[0][0], (float)P[0][1], (float)P[0][2], r[0]);
+    p1[s] = make_float4((float)P[1][0], (float)P[1][1], (float)P[1][2], r[1]);
+    p2[s] = make_float4((float)P[2][0], (float)P[2][1], (float)P[2][2], r[2]);
+    p3[s] = make_float4((float)P[3][0], (float)P[3][1], (float)P[3][2], r[3]);
+    flags[s] = f;
+  }
+}
+
+}  // namespace
+
+extern "C" int fiber_build_segments(const float* ctrl_pts, const float* radii, int64_t n,
+                                    fiber_segments* segs, void* cuda_stream) {
+  if (n < 0 || n >= ((int64_t)1 << 32) || !segs || segs->n != n)
+    return set_error(FIBER_EINVAL, "fiber_build_segments: bad size or descriptor");
+  if (n > 0 && (!ctrl_pts || !radii || !segs->p0 || !segs->p1 || !segs->p2 || !segs->p3 ||
+                !segs->flags))
+    return set_error(FIBER_EINVAL, "fiber_build_segments: NULL pointer");
+  int rc = check_device();
+  if (rc != FIBER_OK) return rc;
+  if (n == 0) return FIBER_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  build_segments_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)cuda_stream>>>(
+      ctrl_pts, radii, n, (float4*)segs->p0, (float4*)segs->p1, (float4*)segs->p2,
+      (float4*)segs->p3, segs->flags);
+  return check_launch("fiber_build_segments");
+}

@@ -1,0 +1,219 @@
+"""Thin Python binding of libfiber.so (include/fiber.h).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of libfiber.so.
+PyTorch is used for device memory and streams.  There is no CPU fallback: if the library or
+a B200 is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfiber.so")
+
+FIBER_OK, FIBER_EINVAL, FIBER_ECUDA, FIBER_EDEVICE = 0, -1, -2, -3
+MAX_DEPTH = 23
+HIT = 1 << 0
+KIND_SHIFT = 1
+KIND_LATERAL, KIND_CAP0, KIND_CAP1, KIND_WEDGE = 0, 1, 2, 3
+INSIDE = 1 << 3
+BAD_INPUT = 1 << 4
+BAD_SEGMENT = 1 << 5
+
+# every symbol include/fiber.h declares
+EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
+           "fiber_intersect", "fiber_intersect_nearest", "fiber_nearest_init",
+           "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
+
+
+class FiberError(RuntimeError):
+    pass
+
+
+class _Segs(ctypes.Structure):
+    _fields_ = [("p0", ctypes.c_void_p), ("p1", ctypes.c_void_p), ("p2", ctypes.c_void_p),
+                ("p3", ctypes.c_void_p), ("flags", ctypes.c_void_p), ("n", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfiber.so (built in-tree by paper_1811_03374_b200.build); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FiberError(f"{LIB_PATH} is missing: run `python -m paper_1811_03374_b200.build`"
+                             " (there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64 = ctypes.c_void_p, ctypes.c_int64
+        L.fiber_segments_bytes.argtypes = [i64]
+        L.fiber_segments_bytes.restype = ctypes.c_size_t
+        L.fiber_segments_view.argtypes = [vp, i64, ctypes.POINTER(_Segs)]
+        L.fiber_build_segments.argtypes = [vp, vp, i64, ctypes.POINTER(_Segs), vp]
+        L.fiber_intersect.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp,
+                                      vp]
+        L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
+                                              ctypes.c_int, vp, vp, vp]
+        L.fiber_nearest_init.argtypes = [vp, i64, vp]
+        for f in ("fiber_segments_view", "fiber_build_segments", "fiber_intersect",
+                  "fiber_intersect_nearest", "fiber_nearest_init", "fiber_abi_version"):
+            getattr(L, f).restype = ctypes.c_int
+        L.fiber_error_string.argtypes = [ctypes.c_int]
+        L.fiber_error_string.restype = ctypes.c_char_p
+        L.fiber_decode_normal.argtypes = [ctypes.c_uint32, ctypes.POINTER(ctypes.c_float)]
+        L.fiber_decode_normal.restype = None
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != FIBER_OK:
+        raise FiberError(f"{what}: {lib().fiber_error_string(rc).decode()} (code {rc})")
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _dev(t: torch.Tensor, dtype, shape_tail, name):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise FiberError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise FiberError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape[1:]) != tuple(shape_tail):
+        raise FiberError(f"{name} must have shape [n, {', '.join(map(str, shape_tail))}]")
+    return t.contiguous()
+
+
+class Segments:
+    """Device SoA segment set (fiber_segments) and the storage that owns it."""
+
+    def __init__(self, n: int, device):
+        self.n = int(n)
+        nbytes = int(lib().fiber_segments_bytes(self.n))
+        self.storage = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        self.desc = _Segs()
+        _check(lib().fiber_segments_view(self.storage.data_ptr(), self.n, ctypes.byref(self.desc)),
+               "fiber_segments_view")
+
+    def flags(self) -> torch.Tensor:
+        off = self.desc.flags - self.storage.data_ptr()
+        return self.storage[off:off + 4 * self.n].view(torch.int32)
+
+    def planes(self) -> list[torch.Tensor]:
+        out = []
+        for p in (self.desc.p0, self.desc.p1, self.desc.p2, self.desc.p3):
+            off = p - self.storage.data_ptr()
+            out.append(self.storage[off:off + 16 * self.n].view(torch.float32).view(self.n, 4))
+        return out
+
+
+def build_segments(ctrl: torch.Tensor, radii: torch.Tensor, stream=None) -> Segments:
+    """fiber_build_segments: ctrl f32[n,4,3], radii f32[n,4] (CUDA) -> Segments."""
+    ctrl = _dev(ctrl, torch.float32, (4, 3), "ctrl")
+    radii = _dev(radii, torch.float32, (4,), "radii")
+    if radii.shape[0] != ctrl.shape[0]:
+        raise FiberError("ctrl and radii disagree on n")
+    segs = Segments(ctrl.shape[0], ctrl.device)
+    _check(lib().fiber_build_segments(ctrl.data_ptr(), radii.data_ptr(), segs.n,
+                                      ctypes.byref(segs.desc), _stream(stream)),
+           "fiber_build_segments")
+    segs._keep = (ctrl, radii)
+    return segs
+
+
+def _pairs(pairs: torch.Tensor) -> torch.Tensor:
+    if pairs.dtype in (torch.int64, torch.uint32):
+        pairs = pairs.to(torch.int32)
+    return _dev(pairs, torch.int32, (2,), "pairs")
+
+
+def intersect(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
+              hits: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """fiber_intersect: rays f32[n_rays,8], pairs i32[n_pairs,2] (CUDA) -> hits f32[n_pairs,4]
+    (t, u, n_oct bits, flags bits); see unpack()."""
+    rays = _dev(rays, torch.float32, (8,), "rays")
+    pairs = _pairs(pairs)
+    if hits is None:
+        hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=rays.device)
+    _check(lib().fiber_intersect(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                 pairs.data_ptr(), pairs.shape[0], int(depth), hits.data_ptr(),
+                                 _stream(stream)), "fiber_intersect")
+    return hits
+
+
+def intersect_nearest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
+                      nearest: torch.Tensor, hits: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """fiber_intersect_nearest: also atomically keeps, per ray, min((t bits << 32) | pair)."""
+    rays = _dev(rays, torch.float32, (8,), "rays")
+    pairs = _pairs(pairs)
+    if nearest.dtype != torch.int64 or nearest.shape != (rays.shape[0],):
+        raise FiberError("nearest must be int64[n_rays]")
+    _check(lib().fiber_intersect_nearest(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                         pairs.data_ptr(), pairs.shape[0], int(depth),
+                                         hits.data_ptr() if hits is not None else None,
+                                         nearest.data_ptr(), _stream(stream)),
+           "fiber_intersect_nearest")
+    return nearest
+
+
+def nearest_init(nearest: torch.Tensor, stream=None) -> torch.Tensor:
+    _check(lib().fiber_nearest_init(nearest.data_ptr(), nearest.numel(), _stream(stream)),
+           "fiber_nearest_init")
+    return nearest
+
+
+# ------------------------------------------------------------------------- host helpers
+def decode_normals(n_oct: np.ndarray) -> np.ndarray:
+    """Vectorised octahedral snorm16x2 decode (same convention as fiber_decode_normal)."""
+    n_oct = np.asarray(n_oct).view(np.uint32)
+    x = (n_oct & 0xFFFF).astype(np.uint16).view(np.int16).astype(np.float64) / 32767.0
+    y = (n_oct >> 16).astype(np.uint16).view(np.int16).astype(np.float64) / 32767.0
+    z = 1.0 - np.abs(x) - np.abs(y)
+    neg = z < 0
+    ox = (1.0 - np.abs(y)) * np.where(x >= 0, 1.0, -1.0)
+    oy = (1.0 - np.abs(x)) * np.where(y >= 0, 1.0, -1.0)
+    x = np.where(neg, ox, x)
+    y = np.where(neg, oy, y)
+    v = np.stack([x, y, z], -1)
+    return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+
+def unpack(hits) -> dict:
+    """hits f32[n,4] (torch or numpy) -> dict(t, u, n[n,3], flags, hit, kind, inside,
+    bad_input, bad_segment, backtracks, tests) as numpy arrays."""
+    h = hits.detach().cpu().numpy() if isinstance(hits, torch.Tensor) else np.asarray(hits)
+    h = np.ascontiguousarray(h, dtype=np.float32)
+    bits = h.view(np.uint32)
+    flags = bits[:, 3]
+    return {
+        "t": h[:, 0].astype(np.float64), "u": h[:, 1].astype(np.float64),
+        "n": decode_normals(bits[:, 2]), "flags": flags,
+        "hit": (flags & HIT) != 0, "kind": ((flags >> KIND_SHIFT) & 3).astype(np.int32),
+        "inside": (flags & INSIDE) != 0, "bad_input": (flags & BAD_INPUT) != 0,
+        "bad_segment": (flags & BAD_SEGMENT) != 0,
+        "backtracks": ((flags >> 8) & 0xFF).astype(np.int32),
+        "tests": ((flags >> 16) & 0xFFFF).astype(np.int32),
+    }
+
+
+def pack_rays(rays_np: np.ndarray, device="cuda") -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(rays_np, dtype=np.float32)).to(device)
+
+
+def to_device(workload, device="cuda"):
+    """Move a workloads.gen.Workload to the GPU: (rays, Segments, pairs)."""
+    rays = torch.from_numpy(np.ascontiguousarray(workload.rays)).to(device)
+    ctrl = torch.from_numpy(np.ascontiguousarray(workload.ctrl)).to(device)
+    radii = torch.from_numpy(np.ascontiguousarray(workload.radii)).to(device)
+    pairs = torch.from_numpy(np.ascontiguousarray(workload.pairs).view(np.int32)).to(device)
+    segs = build_segments(ctrl, radii)
+    return rays, segs, pairs

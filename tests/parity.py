@@ -1,0 +1,61 @@
+"""GPU-vs-oracle comparison (test infrastructure; used by tests and __graft_entry__.smoke).
+
+Bar (BASELINE.json north_star): outside the grazing band the hit flag is
+bit-exact; on pairs whose oracle value is well-conditioned at the eps scale, |t - t_o| <=
+1e-4 |t_o|, |u - u_o| <= 1e-3, angle(n, n_o) <= 1e-3 rad, and the hit kind agrees.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TOL_T, TOL_U, TOL_N = 1e-4, 1e-3, 1e-3
+
+
+def _angle(a, b):
+    c = np.clip(np.sum(a * b, -1) / (np.linalg.norm(a, axis=-1) * np.linalg.norm(b, axis=-1)),
+                -1, 1)
+    return np.arccos(c)
+
+
+def oracle_kind_to_gpu(kind):
+    # oracle: 0 lateral, 1 cap0, 2 cap1, 3 wedge, 4 inside; gpu: kind bits + INSIDE flag
+    return np.where(kind == 4, 0, kind)
+
+
+def compare(g: dict, o: dict) -> dict:
+    """g = paper_1811_03374_b200.unpack(hits); o = oracle.intersect(..., with_eps=True)."""
+    n = o["hit"].shape[0]
+    grazing = o["grazing"]
+    hit_mis = (g["hit"] != o["hit"]) & ~grazing
+    both = g["hit"] & o["hit"]
+    p, m = o["plus"], o["minus"]
+    with np.errstate(invalid="ignore"):
+        stable = (~o["kind_unstable"]) & (p["kind"] == m["kind"])
+        stable &= np.abs(p["t"] - m["t"]) <= TOL_T * np.abs(o["t"])
+        stable &= np.abs(p["u"] - m["u"]) <= TOL_U
+        stable &= _angle(p["n"], m["n"]) <= TOL_N
+    cmp = both & stable & ~grazing
+    with np.errstate(invalid="ignore", divide="ignore"):
+        t_rel = np.where(cmp, np.abs(g["t"] - o["t"]) / np.maximum(np.abs(o["t"]), 1e-30), 0)
+        u_abs = np.where(cmp, np.abs(g["u"] - o["u"]), 0)
+        ang = np.where(cmp, _angle(g["n"], o["n"]), 0)
+    kind_mis = cmp & ((g["kind"] != oracle_kind_to_gpu(o["kind"])) |
+                      (g["inside"] != (o["kind"] == 4)))
+    bad = cmp & ((t_rel > TOL_T) | (u_abs > TOL_U) | (ang > TOL_N) | kind_mis)
+    return {
+        "n": n, "hits": int(o["hit"].sum()), "grazing": int(grazing.sum()),
+        "hit_mismatch": int(hit_mis.sum()), "compared": int(cmp.sum()),
+        "excluded_values": int((both & ~cmp).sum()),
+        "value_mismatch": int(bad.sum()), "kind_mismatch": int(kind_mis.sum()),
+        "max_t_rel": float(t_rel.max()) if n else 0.0, "max_u": float(u_abs.max()) if n else 0.0,
+        "max_angle": float(ang.max()) if n else 0.0,
+        "hit_mismatch_idx": np.flatnonzero(hit_mis)[:10].tolist(),
+        "value_mismatch_idx": np.flatnonzero(bad)[:10].tolist(),
+    }
+
+
+def assert_parity(rep: dict, max_excluded_frac: float = 0.05):
+    assert rep["hit_mismatch"] == 0, rep
+    assert rep["value_mismatch"] == 0, rep
+    if rep["hits"] > 100:
+        assert rep["excluded_values"] + rep["grazing"] <= max_excluded_frac * max(rep["hits"], 1), rep

@@ -1,0 +1,65 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the FP64 oracle on the same seeded
+inputs, element by element.  Needs a B200."""
+import numpy as np
+import pytest
+
+import oracle
+from tests.parity import assert_parity, compare
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fx():
+    import torch
+
+    import paper_1811_03374_b200 as fx
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return fx
+
+
+def _run(fx, w, depth=None):
+    depth = w.depth if depth is None else depth
+    rays, segs, pairs = fx.to_device(w)
+    hits = fx.intersect(rays, segs, pairs, depth)
+    return fx.unpack(hits)
+
+
+def _oracle(w, depth=None):
+    return oracle.intersect(w.rays, w.ctrl, w.radii, w.pairs, w.depth if depth is None else depth)
+
+
+def test_config1_parity(fx):
+    w = gen.config1()
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+    assert rep["hits"] > 300
+
+
+@pytest.mark.parametrize("fiber", ["A", "B", "C"])
+@pytest.mark.parametrize("depth", [2, 3, 4, 6, 9, 12, 16, 20, 22])
+def test_config2_parity_depth_sweep(fx, fiber, depth):
+    w = gen.config2(fiber, n_rays=1 << 15, depth=depth)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+
+
+@pytest.mark.parametrize("depth", [4, 9, 22])
+def test_config2_targeted_parity(fx, depth):
+    w = gen.config2("A", n_rays=1 << 14, depth=depth, targeted=True)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+
+
+def test_spec_example_all_depths(fx):
+    ctrl, radii = gen.straight_fiber()
+    rays = np.array([[3, 0, -5, np.inf, 0, 0, 1, 0]], np.float32)
+    for D in range(0, 24):
+        w = gen.Workload("spec", rays, ctrl, radii, gen.make_pairs_1seg(1), D)
+        g = _run(fx, w)
+        assert g["hit"][0]
+        assert abs(g["t"][0] - 4.9) < 1e-5 and abs(g["u"][0] - 0.5) < 1e-6
+        assert np.allclose(g["n"][0], [0, 0, -1], atol=1e-4)
