@@ -322,7 +322,7 @@ def _time_oracle(ws, nthreads):
     return n, time.perf_counter() - t0
 
 
-def cpu_baseline(n_per: int = 1 << 14):
+def cpu_baseline(n_per: int = 1 << 17):
     import oracle
 
     oracle.build()

@@ -28,21 +28,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple[str, ...] = ()) -> str:
+    """Build libfiber.so (or a test variant at `out` with extra -D defines)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-shared", *srcs,
-           "-o", LIB + ".tmp"]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I",
+           CSRC, "-shared", *srcs, "-o", lib + ".tmp"]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         sys.stderr.write(p.stdout + p.stderr)
         raise RuntimeError("nvcc failed building libfiber.so")
     if verbose:
         sys.stderr.write(p.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    if "--variants" in sys.argv:  # test builds (IEEE-rounded FP32 math)
+        build(force=True, out=os.path.join(HERE, "libfiber_ieee.so"), defines=("FIBER_IEEE_MATH",))
+        build(force=True, out=os.path.join(HERE, "libfiber_trace.so"), defines=("FIBER_TRACE",))

@@ -17,9 +17,17 @@ int set_error(int code, const char* msg) {
 }
 
 int check_device() {
+  // the compute capability of each device, queried once (immutable)
+  static int major_of[64];
   int dev = 0, major = 0;
   cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e == cudaSuccess && dev >= 0 && dev < 64 && __atomic_load_n(&major_of[dev], __ATOMIC_ACQUIRE))
+    major = major_of[dev];
+  else if (e == cudaSuccess) {
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e == cudaSuccess && dev >= 0 && dev < 64)
+      __atomic_store_n(&major_of[dev], major, __ATOMIC_RELEASE);
+  }
   if (e != cudaSuccess) {
     char buf[400];
     snprintf(buf, sizeof(buf), "CUDA: %s", cudaGetErrorString(e));

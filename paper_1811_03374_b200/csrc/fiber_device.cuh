@@ -4,11 +4,9 @@
 // implements; DESIGN.md "Kernel" explains what differs from the paper's listings and why.
 //
 // Split of precision:
-//   a2 setup      FP64: origin shifted onto the ray next to the segment, ONB, transform to
-//                 the unit-ray frame, rounded once to FP32.
-//   a3-a6 loop    FP32: node test / descend / backtrack, the paper's hot loop.
-//   a7 finalise   FP64: re-solve of the accepted leaf (walking to the neighbour leaf the
-//                 ray really enters when FP32 picked a neighbour at D >= 18).
+//   a2 setup      FP32 frame whose origin shift is formed in FP64 (intersect.cu).
+//   a3-a6 loop    FP32: node test / descend / backtrack, the paper's hot loop (this file).
+//   a7 finalise   FP64: re-solve of the accepted leaf (intersect.cu, kernel K3).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -42,78 +40,27 @@ __device__ __forceinline__ float cross_norm2(float4 a, float4 b) {
   return fmaf(cx, cx, fmaf(cy, cy, cz * cz));
 }
 
-// ------------------------------------------------------------------------------------
-// FP64 helpers
-// ------------------------------------------------------------------------------------
-struct d3 {
-  double x, y, z;
-};
-struct d4 {
-  double x, y, z, w;
-};
-__device__ __forceinline__ d3 mk3(double x, double y, double z) { return d3{x, y, z}; }
-__device__ __forceinline__ d3 sub(d3 a, d3 b) { return d3{a.x - b.x, a.y - b.y, a.z - b.z}; }
-__device__ __forceinline__ double dot(d3 a, d3 b) {
-  return fma(a.x, b.x, fma(a.y, b.y, a.z * b.z));
+// Approximate MUFU intrinsics (<= 2 ulp); the parity tolerances absorb them.
+// -DFIBER_IEEE_MATH builds the IEEE-rounded variant (a test build, never the product).
+#ifdef FIBER_IEEE_MATH
+__device__ __forceinline__ float fsqrt(float x) { return __fsqrt_rn(x); }
+__device__ __forceinline__ float frcp(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+#else
+// .ftz: operands here are never subnormal (coordinates are normalised by the frame shift),
+// and flushing drops the range fix-ups the non-ftz forms compile to.
+__device__ __forceinline__ float fsqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-__device__ __forceinline__ d4 add4(d4 a, d4 b) { return d4{a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w}; }
-__device__ __forceinline__ d4 sub4(d4 a, d4 b) { return d4{a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w}; }
-__device__ __forceinline__ d4 mul4(double s, d4 a) { return d4{s * a.x, s * a.y, s * a.z, s * a.w}; }
-__device__ __forceinline__ d4 fma4(double s, d4 a, d4 b) {
-  return d4{fma(s, a.x, b.x), fma(s, a.y, b.y), fma(s, a.z, b.z), fma(s, a.w, b.w)};
+__device__ __forceinline__ float frcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-__device__ __forceinline__ float4 to_f4(d4 a) {
-  return make_float4((float)a.x, (float)a.y, (float)a.z, (float)a.w);
-}
-
-// Orthonormal basis around a unit vector w: Duff et al. 2017's revision of Frisvad's
-// construction, named by the paper at P:476-477 (the listing calls make_ONB).
-__device__ __forceinline__ void make_onb(d3 w, d3& b1, d3& b2) {
-  double sign = copysign(1.0, w.z);
-  double a = -1.0 / (sign + w.z);
-  double b = w.x * w.y * a;
-  b1 = mk3(1.0 + sign * w.x * w.x * a, sign * b, -sign * w.x);
-  b2 = mk3(b, sign + w.y * w.y * a, -w.y);
-}
-
-// ------------------------------------------------------------------------------------
-// Per-pair frame (a2).  World point X maps to local (<X-o', b1>, <X-o', b2>, <X-o', w^>)
-// with o' = o + ts w^ on the ray next to the segment (ts = <c - o, w^>, c = (P0 + P3)/2):
-// the ray becomes the unit ray (0,0,0) + s (0,0,1) of P:475-481, and local coordinates are
-// small, so their FP32 rounding is relative to the segment size, not to |o - P|.
-// ------------------------------------------------------------------------------------
-struct Frame {
-  d3 o;        // o' (world)
-  d3 b1, b2, w;  // orthonormal frame, w = d / |d|
-  double ts;   // o' = o + ts * w (distance units)
-  double lw;   // |d|: t = s / |d|
-};
-
-// Returns false for a degenerate ray (non-finite values, zero direction, tmax <= 0).
-__device__ __forceinline__ bool make_frame(const float4 ray0, const float4 ray1, const float4 P0,
-                                           const float4 P3, Frame& F) {
-  d3 o = mk3(ray0.x, ray0.y, ray0.z);
-  d3 d = mk3(ray1.x, ray1.y, ray1.z);
-  double lw = sqrt(dot(d, d));
-  bool ok = isfinite(ray0.x) && isfinite(ray0.y) && isfinite(ray0.z) && isfinite(ray1.x) &&
-            isfinite(ray1.y) && isfinite(ray1.z) && !(ray0.w <= 0.0f) && !isnan(ray0.w) &&
-            lw > 0.0;
-  if (!ok) lw = 1.0, d = mk3(0, 0, 1);
-  double il = 1.0 / lw;
-  F.w = mk3(d.x * il, d.y * il, d.z * il);
-  F.lw = lw;
-  make_onb(F.w, F.b1, F.b2);
-  d3 c = mk3(0.5 * ((double)P0.x + (double)P3.x), 0.5 * ((double)P0.y + (double)P3.y),
-             0.5 * ((double)P0.z + (double)P3.z));
-  F.ts = dot(sub(c, o), F.w);
-  F.o = mk3(fma(F.ts, F.w.x, o.x), fma(F.ts, F.w.y, o.y), fma(F.ts, F.w.z, o.z));
-  return ok;
-}
-
-__device__ __forceinline__ d4 to_local(const Frame& F, float4 P) {
-  d3 q = sub(mk3(P.x, P.y, P.z), F.o);
-  return d4{dot(q, F.b1), dot(q, F.b2), dot(q, F.w), (double)P.w};
-}
+__device__ __forceinline__ float fdiv(float a, float b) { return a * frcp(b); }
+#endif
 
 // ------------------------------------------------------------------------------------
 // Curve in the (p, d, t0, t1) representation of 3.1, FP32.
@@ -170,32 +117,53 @@ enum : uint32_t { TAG_ORIGIN = 0, TAG_START = 1, TAG_END = 2, TAG_INTERNAL = 3 }
 // The node's own slab: [lo0, hi0] cut by the start plane (through p, normal t0, keeps
 // <x - p, t0> >= 0) and the end plane (through p + d, normal t1, keeps <x - p - d, t1> <= 0)
 // -- lst:calc_t_interval P:1459-1477 with F3 (a plane parallel to the ray keeps all or
-// nothing) and F7 (t_max passed explicitly).  tag: what bounds t_min.
+// nothing) and F7 (t_max passed explicitly).  tag: what bounds t_min.  `widen` moves the
+// two planes outward by a bound on their FP32 rounding error: used after a node was
+// RE-COMPUTED (lst:recalculation), whose planes can sit a few ulps off the ones the
+// sibling's interval was cut with; without it a hit on the shared plane could fall into
+// the gap between the two intervals.
 __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, bool u0_is_0,
-                                     bool u1_is_1, float& tmin, float& tmax, uint32_t& tag) {
+                                     bool u1_is_1, float& tmin, float& tmax, uint32_t& tag,
+                                     bool widen = false) {
   tmin = lo0;
   tmax = hi0;
   tag = TAG_ORIGIN;
   float n0 = dot3(c.t0, c.p), z0 = c.t0.z;
   float4 e = c.p + c.d;
   float n1 = dot3(c.t1, e), z1 = c.t1.z;
+  if (widen) {
+    // |error of <t, x>| <~ 2^-20 (|t| . |x|) covers the dot product and the recomputed x
+    const float k = 9.5367431640625e-07f;  // 2^-20
+    float a0 = fmaf(fabsf(c.t0.x), fabsf(c.p.x), fmaf(fabsf(c.t0.y), fabsf(c.p.y), fabsf(c.t0.z) * fabsf(c.p.z)));
+    float a1 = fmaf(fabsf(c.t1.x), fabsf(e.x), fmaf(fabsf(c.t1.y), fabsf(e.y), fabsf(c.t1.z) * fabsf(e.z)));
+    n0 -= k * a0;  // start plane moved against t0 (outward)
+    n1 += k * a1;  // end plane moved along t1 (outward)
+  }
   if (z0 > 0.0f) {
-    float x = n0 / z0;
+    float x = fdiv(n0, z0);
     if (x > tmin) tmin = x, tag = u0_is_0 ? TAG_START : TAG_INTERNAL;
   } else if (z0 < 0.0f) {
-    tmax = fminf(tmax, n0 / z0);
+    tmax = fminf(tmax, fdiv(n0, z0));
   } else if (n0 > 0.0f) {
     tmin = INFINITY;  // parallel and on the invalid side: empty
   }
   if (z1 < 0.0f) {
-    float x = n1 / z1;
+    float x = fdiv(n1, z1);
     if (x > tmin) tmin = x, tag = u1_is_1 ? TAG_END : TAG_INTERNAL;
   } else if (z1 > 0.0f) {
-    tmax = fminf(tmax, n1 / z1);
+    tmax = fminf(tmax, fdiv(n1, z1));
   } else if (n1 < 0.0f) {
     tmin = INFINITY;
   }
 }
+
+// Descent-time crop limit: partition planes crop the ray interval
+// only down to level kCropLevel.  Below it a level's slab along the ray (~2^-l of the
+// segment) falls under FP32 resolution of the plane crossings, so its bounds would invert
+// by rounding; deeper nodes inherit the level-kCropLevel interval, and the planes still
+// order the children.  The FP64 finalisation then re-solves the exact leaf.
+constexpr int kCropLevel = 15;
+constexpr uint32_t kCropMinSize = 1u << (FIBER_MAX_DEPTH - kCropLevel);
 
 // Node test (a3): conservative radius (lst:calc_radius P:1415-1425 with the point-line
 // distance of lst:distance-point-line P:1308-1328, here |t x d|^2 / |d|^2) and the unit ray
@@ -205,79 +173,71 @@ __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, bool 
 __device__ __forceinline__ bool cylinder(const Delta& c, float& c0, float& c1) {
   float dd = dot3(c.d, c.d);
   float m2 = fmaxf(cross_norm2(c.t0, c.d), cross_norm2(c.t1, c.d));
-  float dist = sqrtf(m2 / dd);
+  float dist = fsqrt(m2 * frcp(dd));
   float maxr = c.p.w + fmaxf(fmaxf(0.0f, c.t0.w), fmaxf(c.d.w, c.d.w - c.t1.w));
   float R = dist + maxr;
   float g = fmaf(c.d.x, c.d.x, c.d.y * c.d.y);
-  if (g <= 1e-12f * dd) {
-    c0 = -INFINITY;
-    c1 = INFINITY;
-    return fmaf(c.p.x, c.p.x, c.p.y * c.p.y) <= R * R;
-  }
-  float h = 1.0f / g;
-  float dxy = c.d.x * c.p.y - c.d.y * c.p.x;
+  float h = frcp(g);
+  float dxy = fmaf(c.d.x, c.p.y, -c.d.y * c.p.x);
   float e = fmaf(R, R, -dxy * dxy * h);
-  float tc = c.p.z - c.d.z * fmaf(c.d.x, c.p.x, c.d.y * c.p.y) * h;
-  float s = sqrtf(e * fmaf(c.d.z, c.d.z, g) * h);
-  c0 = tc - s;
-  c1 = tc + s;
-  return e >= 0.0f;
+  float tc = fmaf(-c.d.z * h, fmaf(c.d.x, c.p.x, c.d.y * c.p.y), c.p.z);
+  float s = fsqrt(e * fmaf(c.d.z, c.d.z, g) * h);
+  // F4 (selects, no branch): axis parallel to the ray -> whole line if inside, else empty
+  bool par = g <= 1e-12f * dd;
+  bool in = fmaf(c.p.x, c.p.x, c.p.y * c.p.y) <= R * R;
+  c0 = par ? -INFINITY : tc - s;
+  c1 = par ? INFINITY : tc + s;
+  return par ? in : (e >= 0.0f);
 }
 
 // Descend (a4): split point and tangent of 3.1, partition plane through
 // p + delta_p with normal t_c (lst:ray-plane P:1246-1251), near child first
 // (P:1444 as XOR, F9), both-hit on the uncropped cylinder interval,
-// one-bound update, child by the delta rules (lst:subdivide P:1391-1412).
-// F3: a partition plane parallel to the ray: near child = the side of the ray, no both,
-// no update.
-__device__ __forceinline__ void descend(Delta& c, float c0, float c1, float& tmin, float& tmax,
-                                        uint32_t& tag, bool& right, bool& both) {
-  float4 dp = 0.375f * (c.t0 - c.t1) + 0.5f * c.d;
-  float4 tcn = 0.25f * c.d - 0.125f * (c.t0 + c.t1);
-  float4 S = c.p + dp;
-  float num = dot3(tcn, S), nz = tcn.z;
-  if (nz != 0.0f) {
-    float tP = num / nz;
-    right = (tP > c0) != (nz > 0.0f);
-    both = (c0 < tP) && (tP < c1);
-    if (tP > c0) {
-      tmax = fminf(tmax, tP);
-    } else if (tP > tmin) {
-      tmin = tP;
-      tag = TAG_INTERNAL;
-    }
-  } else {
-    right = num < 0.0f;
-    both = false;
-  }
-  if (right) {
-    c.p = S;
-    c.d = c.d - dp;
-    c.t0 = tcn;
-    c.t1 = 0.5f * c.t1;
-  } else {
-    c.d = dp;
-    c.t0 = 0.5f * c.t0;
-    c.t1 = tcn;
-  }
+// one-bound update while `crop`.  F3: a partition plane parallel to the
+// ray: near child = the side of the ray, no both, no update.  The children follow the
+// delta rules of lst:subdivide P:1391-1412:
+//   left = (p, dp, t0/2, t_c),   right = (p + dp, d - dp, t_c, t1/2).
+struct Split {
+  float4 dp, tcn, S;
+  bool right, both;
+};
+
+// Split point and tangent of node c (3.1): delta_p, t_c and S = p + delta_p.
+__device__ __forceinline__ void split_geometry(const Delta& c, Split& sp) {
+  sp.dp = 0.375f * (c.t0 - c.t1) + 0.5f * c.d;
+  sp.tcn = 0.25f * c.d - 0.125f * (c.t0 + c.t1);
+  sp.S = c.p + sp.dp;
 }
 
-// ------------------------------------------------------------------------------------
-// Octahedral normal encoding, 2 x snorm16 (decode error < 6e-5 rad).
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t encode_oct(double nx, double ny, double nz) {
-  double l1 = fabs(nx) + fabs(ny) + fabs(nz);
-  if (!(l1 > 0.0)) return 0u;
-  double x = nx / l1, y = ny / l1;
-  if (nz < 0.0) {
-    double ox = (1.0 - fabs(y)) * copysign(1.0, x);
-    double oy = (1.0 - fabs(x)) * copysign(1.0, y);
-    x = ox;
-    y = oy;
-  }
-  int ix = __double2int_rn(fmin(1.0, fmax(-1.0, x)) * 32767.0);
-  int iy = __double2int_rn(fmin(1.0, fmax(-1.0, y)) * 32767.0);
-  return ((uint32_t)ix & 0xffffu) | (((uint32_t)iy & 0xffffu) << 16);
+__device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, float& tmin,
+                                           float& tmax, uint32_t& tag, bool crop) {
+  Split sp;
+  split_geometry(c, sp);
+  float num = dot3(sp.tcn, sp.S), nz = sp.tcn.z;
+  float tP = num * frcp(nz);
+  bool par = (nz == 0.0f);
+  sp.right = par ? (num < 0.0f) : ((tP > c0) != (nz > 0.0f));
+  sp.both = !par && (c0 < tP) && (tP < c1);
+  bool up = tP > c0;
+  bool apply = crop && !par;
+  tmax = (apply && up) ? fminf(tmax, tP) : tmax;
+  bool lo_up = apply && !up && (tP > tmin);
+  tmin = lo_up ? tP : tmin;
+  tag = lo_up ? (uint32_t)TAG_INTERNAL : tag;
+  return sp;
+}
+
+// The child on side `right` of the split (selects only).
+__device__ __forceinline__ void child(const Delta& c, const Split& sp, bool right, Delta& out) {
+#define FX_SEL4(dst, a, b)                                                             \
+  dst = make_float4(right ? (a).x : (b).x, right ? (a).y : (b).y, right ? (a).z : (b).z, \
+                    right ? (a).w : (b).w)
+  float4 rd = c.d - sp.dp, h0 = 0.5f * c.t0, h1 = 0.5f * c.t1;
+  FX_SEL4(out.p, sp.S, c.p);
+  FX_SEL4(out.d, rd, sp.dp);
+  FX_SEL4(out.t0, sp.tcn, h0);
+  FX_SEL4(out.t1, h1, sp.tcn);
+#undef FX_SEL4
 }
 
 }  // namespace fiberx

@@ -7,6 +7,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <atomic>
+#include <mutex>
 
 #include "fiber.h"
 #include "fiber_device.cuh"
@@ -14,248 +17,617 @@
 
 namespace fiberx {
 
-// ------------------------------------------------------------------------------------
-// FP64 leaf geometry for finalisation (a7)
-// ------------------------------------------------------------------------------------
-struct LeafD {
-  d4 p, d, t0, t1;
-};
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kQueue = 64;  // K3 per-warp queue capacity (<= 31 left + 32 new)
+constexpr int kFarCache = 2;  // per-lane cache of pending far children
+constexpr size_t kSmemBytes = (size_t)(4 + 4 * kFarCache) * kThreads * sizeof(float4);
 
-__device__ __forceinline__ d4 hblossom_d(const d4 D[3], double a, double b) {
-  double wa = (1.0 - a) * (1.0 - b), wb = a * (1.0 - b) + (1.0 - a) * b, wc = a * b;
-  return d4{wa * D[0].x + wb * D[1].x + wc * D[2].x, wa * D[0].y + wb * D[1].y + wc * D[2].y,
-            wa * D[0].z + wb * D[1].z + wc * D[2].z, wa * D[0].w + wb * D[1].w + wc * D[2].w};
+// ------------------------------------------------------------------------------------
+// a7: FP64 finalisation (lst:calc_intersection P:1546-1587 with F2, F6, F8)
+// ------------------------------------------------------------------------------------
+// World coordinates relative to the segment anchor c = fl((P0 + P3)/2): every input is an
+// FP32 number, so differences are exact or nearly so in FP64 and no frame is needed.
+struct D4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ D4 d4of(float4 a) { return D4{a.x, a.y, a.z, a.w}; }
+__device__ __forceinline__ D4 dsub(D4 a, D4 b) { return D4{a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w}; }
+__device__ __forceinline__ D4 dadd(D4 a, D4 b) { return D4{a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w}; }
+__device__ __forceinline__ D4 dscale(double s, D4 a) { return D4{s * a.x, s * a.y, s * a.z, s * a.w}; }
+__device__ __forceinline__ double ddot3(D4 a, D4 b) { return fma(a.x, b.x, fma(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ D4 dcross(D4 a, D4 b) {
+  return D4{fma(a.y, b.z, -a.z * b.y), fma(a.z, b.x, -a.x * b.z), fma(a.x, b.y, -a.y * b.x), 0.0};
 }
 
-// Sub-curve on [u0, u1] of the local FP64 curve, in the (p, d, t0, t1) form (3.1).
-__device__ __forceinline__ LeafD leaf_d(const d4 L[4], double u0, double u1) {
-  d4 D[3] = {sub4(L[1], L[0]), sub4(L[2], L[1]), sub4(L[3], L[2])};
+struct LeafD {
+  D4 p, d, t0, t1;  // (p, d, t0, t1) form of 3.1, relative to the anchor
+};
+
+// Sub-curve on [u0, u1] from the hodograph blossoms (as recompute(), in FP64).
+__device__ __forceinline__ LeafD leaf_d(D4 q0, D4 D0, D4 D1, D4 D2, double u0, double u1) {
+  auto H = [&](double a, double b) {
+    double wa = (1.0 - a) * (1.0 - b), wb = a * (1.0 - b) + (1.0 - a) * b, wc = a * b;
+    return D4{fma(wa, D0.x, fma(wb, D1.x, wc * D2.x)), fma(wa, D0.y, fma(wb, D1.y, wc * D2.y)),
+              fma(wa, D0.z, fma(wb, D1.z, wc * D2.z)), fma(wa, D0.w, fma(wb, D1.w, wc * D2.w))};
+  };
   double h = u1 - u0;
-  d4 H00 = hblossom_d(D, u0, u0), H01 = hblossom_d(D, u0, u1), H11 = hblossom_d(D, u1, u1);
-  d4 H0u = hblossom_d(D, 0.0, u0);
+  D4 H00 = H(u0, u0), H01 = H(u0, u1), H11 = H(u1, u1), H0u = H(0.0, u0);
+  D4 s = dadd(dadd(D0, H0u), H00);
   LeafD q;
-  q.p = fma4(u0, add4(add4(D[0], H0u), H00), L[0]);
-  q.t0 = mul4(h, H00);
-  q.t1 = mul4(h, H11);
-  q.d = mul4(h, add4(add4(H00, H01), H11));
+  q.p = D4{fma(u0, s.x, q0.x), fma(u0, s.y, q0.y), fma(u0, s.z, q0.z), fma(u0, s.w, q0.w)};
+  q.t0 = dscale(h, H00);
+  q.t1 = dscale(h, H11);
+  q.d = dscale(h, dadd(dadd(H00, H01), H11));
   return q;
 }
 
-__device__ __forceinline__ double cross_n2_d(d4 a, d4 b) {
-  double cx = a.y * b.z - a.z * b.y, cy = a.z * b.x - a.x * b.z, cz = a.x * b.y - a.y * b.x;
-  return cx * cx + cy * cy + cz * cz;
-}
-
-// Unit ray x leaf cylinder in FP64 (App. A), entry c0 of the infinite cylinder.
-__device__ __forceinline__ bool cylinder_d(const LeafD& c, double& c0) {
-  double dd = c.d.x * c.d.x + c.d.y * c.d.y + c.d.z * c.d.z;
-  double m2 = fmax(cross_n2_d(c.t0, c.d), cross_n2_d(c.t1, c.d));
-  double maxr = c.p.w + fmax(fmax(0.0, c.t0.w), fmax(c.d.w, c.d.w - c.t1.w));
+// Entry parameter t of the ray m + t w (m relative to the anchor) into the infinite
+// conservative cylinder of leaf q (App. A's definition), FP64, stable roots.
+__device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t) {
+  double dd = ddot3(q.d, q.d);
+  D4 x0 = dcross(q.t0, q.d), x1 = dcross(q.t1, q.d);
+  double m2 = fmax(ddot3(x0, x0), ddot3(x1, x1));
+  double maxr = q.p.w + fmax(fmax(0.0, q.t0.w), fmax(q.d.w, q.d.w - q.t1.w));
   double R = sqrt(m2 / dd) + maxr;
-  double g = c.d.x * c.d.x + c.d.y * c.d.y;
-  if (!(g > 0.0)) return false;
-  double h = 1.0 / g;
-  double dxy = c.d.x * c.p.y - c.d.y * c.p.x;
-  double e = R * R - dxy * dxy * h;
-  if (!(e >= 0.0)) return false;
-  double tc = c.p.z - c.d.z * (c.d.x * c.p.x + c.d.y * c.p.y) * h;
-  c0 = tc - sqrt(e * (c.d.z * c.d.z + g) * h);
-  return true;
+  D4 mm = dsub(m, q.p);
+  D4 md = dcross(mm, q.d), wd = dcross(w, q.d);
+  double A = ddot3(wd, wd), B = ddot3(md, wd), C = fma(-R * R, dd, ddot3(md, md));
+  double disc = fma(B, B, -A * C);
+  if (!(A > 0.0) || !(disc >= 0.0)) return false;
+  double qq = -(B + copysign(sqrt(disc), B));
+  double r0 = qq / A, r1 = C / qq;
+  t = fmin(r0, r1);
+  return isfinite(t);
 }
 
-// Finalisation (a7, lst:calc_intersection P:1546-1587 with F6, F8).  Re-solves the accepted
-// leaf in FP64 from the input arrays; for lateral hits walks to the neighbouring leaf whose
-// own slab contains the FP64 entry point (the FP32 leaf index can be a few leaves off at
-// D >= 18 because leaves are then narrower than FP32 resolution).
-__device__ __noinline__ void finalize(const float4 ray0, const float4 ray1, const float4 P0,
-                                      const float4 P1, const float4 P2, const float4 P3,
-                                      uint32_t start, int depth, uint32_t kind, float s32,
-                                      float& t_out, float& u_out, uint32_t& n_out,
-                                      bool& hit) {
-  Frame F;
-  make_frame(ray0, ray1, P0, P3, F);
-  d4 L[4] = {to_local(F, P0), to_local(F, P1), to_local(F, P2), to_local(F, P3)};
-  const int sh = FIBER_MAX_DEPTH - depth;
+__device__ __forceinline__ uint32_t encode_oct32(double nx, double ny, double nz) {
+  double mx = fmax(fabs(nx), fmax(fabs(ny), fabs(nz)));
+  if (!(mx > 0.0)) return 0u;
+  float x = (float)(nx / mx), y = (float)(ny / mx), z = (float)(nz / mx);
+  float l1 = fabsf(x) + fabsf(y) + fabsf(z);
+  x /= l1;
+  y /= l1;
+  if (z < 0.0f) {
+    float ox = (1.0f - fabsf(y)) * copysignf(1.0f, x);
+    float oy = (1.0f - fabsf(x)) * copysignf(1.0f, y);
+    x = ox;
+    y = oy;
+  }
+  int ix = __float2int_rn(fminf(1.0f, fmaxf(-1.0f, x)) * 32767.0f);
+  int iy = __float2int_rn(fminf(1.0f, fmaxf(-1.0f, y)) * 32767.0f);
+  return ((uint32_t)ix & 0xffffu) | (((uint32_t)iy & 0xffffu) << 16);
+}
+
+// Re-solves the accepted leaf in FP64.  Lateral entries walk to the neighbouring leaf whose
+// own slab holds the entry point (the FP32 leaf can be a few leaves off at D >= 16, where
+// leaves are narrower than FP32 resolution); cap entries use the global cap plane; crop
+// (WEDGE) and inside entries keep the FP32 parameter t32.
+__device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, const float4 P0,
+                                         const float4 P1, const float4 P2, const float4 P3,
+                                         uint32_t start, int depth, uint32_t kind, float t32,
+                                         float& t_out, float& u_out, uint32_t& n_out,
+                                         bool& hit) {
+  const D4 c = D4{0.5 * ((double)P0.x + (double)P3.x), 0.5 * ((double)P0.y + (double)P3.y),
+                  0.5 * ((double)P0.z + (double)P3.z), 0.0};
+  const D4 q0 = dsub(d4of(P0), c);
+  const D4 D0 = dsub(d4of(P1), d4of(P0)), D1 = dsub(d4of(P2), d4of(P1)), D2 = dsub(d4of(P3), d4of(P2));
+  const D4 m = D4{(double)ray0.x - c.x, (double)ray0.y - c.y, (double)ray0.z - c.z, 0.0};
+  const D4 w = D4{ray1.x, ray1.y, ray1.z, 0.0};
   const int64_t nleaf = (int64_t)1 << depth;
-  int64_t k = (int64_t)(start >> sh);
   const double inv = 1.0 / (double)nleaf;
-  double s = (double)s32, u = 0.0;
-  d3 n = mk3(0, 0, 0);
-  bool world_normal = false;
+  int64_t k = (int64_t)(start >> (FIBER_MAX_DEPTH - depth));
+  double t = (double)t32, u = 0.0;
+  D4 n;
   if (kind == FIBER_KIND_CAP0 || kind == FIBER_KIND_CAP1) {
-    // entry through a global cap plane: the plane of lst:calc_t_interval at u = 0 or 1
-    d4 q = kind == FIBER_KIND_CAP0 ? L[0] : L[3];
-    d4 nn = kind == FIBER_KIND_CAP0 ? sub4(L[1], L[0]) : sub4(L[3], L[2]);
-    if (nn.z != 0.0) s = (q.x * nn.x + q.y * nn.y + q.z * nn.z) / nn.z;
-    u = kind == FIBER_KIND_CAP0 ? 0.0 : 1.0;
-    // cap normal in world space
-    float4 a = kind == FIBER_KIND_CAP0 ? P0 : P3, b = kind == FIBER_KIND_CAP0 ? P1 : P2;
-    n = mk3((double)a.x - b.x, (double)a.y - b.y, (double)a.z - b.z);
-    world_normal = true;
+    // the global cap plane of lst:calc_t_interval at u = 0 / u = 1, cap normal P:1567-1573
+    bool c0k = kind == FIBER_KIND_CAP0;
+    D4 qp = c0k ? q0 : dsub(d4of(P3), c);
+    D4 nn = c0k ? D0 : D2;
+    double wn = ddot3(w, nn);
+    if (wn != 0.0) t = ddot3(dsub(qp, m), nn) / wn;
+    u = c0k ? 0.0 : 1.0;
+    n = c0k ? dscale(-1.0, D0) : D2;
   } else {
-    LeafD q = leaf_d(L, k * inv, (k + 1) * inv);
+    LeafD q = leaf_d(q0, D0, D1, D2, k * inv, (k + 1) * inv);
     if (kind == FIBER_KIND_LATERAL) {
-      double c0;
-      if (cylinder_d(q, c0)) {
-        s = c0;
+      double te;
+      if (leaf_entry(q, m, w, te)) {
+        t = te;
         int dir = 0;
         for (int it = 0; it < 64; ++it) {
           // side of the entry point w.r.t. the leaf's own start / end planes
-          double z0 = s - q.p.z;
-          double side0 = -q.p.x * q.t0.x - q.p.y * q.t0.y + z0 * q.t0.z;
-          double z1 = s - (q.p.z + q.d.z);
-          double side1 = -(q.p.x + q.d.x) * q.t1.x - (q.p.y + q.d.y) * q.t1.y + z1 * q.t1.z;
+          D4 X = dsub(D4{fma(t, w.x, m.x), fma(t, w.y, m.y), fma(t, w.z, m.z), 0.0}, q.p);
+          double side0 = ddot3(X, q.t0);
+          double side1 = ddot3(dsub(X, q.d), q.t1);
           int step = 0;
           if (side0 < 0.0 && k > 0 && dir <= 0) step = -1;
           else if (side1 > 0.0 && k < nleaf - 1 && dir >= 0) step = +1;
           if (step == 0) break;
-          LeafD qn = leaf_d(L, (k + step) * inv, (k + step + 1) * inv);
-          double cn;
-          if (!cylinder_d(qn, cn)) break;
+          LeafD qn = leaf_d(q0, D0, D1, D2, (k + step) * inv, (k + step + 1) * inv);
+          double tn;
+          if (!leaf_entry(qn, m, w, tn)) break;
           k += step;
           dir = step;
           q = qn;
-          s = cn;
+          t = tn;
         }
       }
     }
     // u by projection onto the leaf chord, normal from the axis point (F8)
-    double dd = q.d.x * q.d.x + q.d.y * q.d.y + q.d.z * q.d.z;
-    double ul = ((0.0 - q.p.x) * q.d.x + (0.0 - q.p.y) * q.d.y + (s - q.p.z) * q.d.z) / dd;
+    D4 X = dsub(D4{fma(t, w.x, m.x), fma(t, w.y, m.y), fma(t, w.z, m.z), 0.0}, q.p);
+    double ul = ddot3(X, q.d) / ddot3(q.d, q.d);
     ul = fmin(1.0, fmax(0.0, ul));
-    u = (k + ul) * inv;
-    n = mk3(-(q.p.x + ul * q.d.x), -(q.p.y + ul * q.d.y), s - (q.p.z + ul * q.d.z));
-  }
-  double t = (F.ts + s) / F.lw;
-  if (!world_normal) {
-    n = mk3(n.x * F.b1.x + n.y * F.b2.x + n.z * F.w.x, n.x * F.b1.y + n.y * F.b2.y + n.z * F.w.y,
-            n.x * F.b1.z + n.y * F.b2.z + n.z * F.w.z);
+    u = ((double)k + ul) * inv;
+    n = D4{fma(-ul, q.d.x, X.x), fma(-ul, q.d.y, X.y), fma(-ul, q.d.z, X.z), 0.0};
   }
   hit = t < (double)ray0.w;
   t_out = hit ? (float)t : INFINITY;
   u_out = hit ? (float)u : 0.0f;
-  n_out = hit ? encode_oct(n.x, n.y, n.z) : 0u;
+  n_out = hit ? encode_oct32(n.x, n.y, n.z) : 0u;
 }
 
 // ------------------------------------------------------------------------------------
-// the per-pair traversal
+// a2 setup: FP32 frame with an FP64-exact origin shift
 // ------------------------------------------------------------------------------------
-template <bool kNearest>
-__global__ void __launch_bounds__(256) intersect_kernel(
-    const float4* __restrict__ rays, int64_t n_rays, const float4* __restrict__ sp0,
-    const float4* __restrict__ sp1, const float4* __restrict__ sp2, const float4* __restrict__ sp3,
-    const uint32_t* __restrict__ sflags, int64_t n_segs, const uint2* __restrict__ pairs,
-    int64_t n_pairs, int depth, float4* __restrict__ hits,
-    unsigned long long* __restrict__ nearest) {
-  const uint32_t min_size = 1u << (FIBER_MAX_DEPTH - depth);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pairs;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 pr = __ldg(&pairs[i]);
-    uint32_t flags = 0;
-    float t_out = INFINITY, u_out = 0.0f;
-    uint32_t n_out = 0;
-    if ((int64_t)pr.x >= n_rays || (int64_t)pr.y >= n_segs) {
-      flags = FIBER_BAD_INPUT;
-    } else {
-      const float4 ray0 = __ldg(&rays[2 * (int64_t)pr.x]);
-      const float4 ray1 = __ldg(&rays[2 * (int64_t)pr.x + 1]);
-      const float4 P0 = __ldg(&sp0[pr.y]), P1 = __ldg(&sp1[pr.y]);
-      const float4 P2 = __ldg(&sp2[pr.y]), P3 = __ldg(&sp3[pr.y]);
-      if (__ldg(&sflags[pr.y]) != 0u) flags |= FIBER_BAD_SEGMENT;
-      // ---- a2: FP64 setup: frame, transform (lst:transform_curve P:1482-1512), rounding
-      Frame F;
-      bool ok = make_frame(ray0, ray1, P0, P3, F);
-      if (!ok) {
-        flags |= FIBER_BAD_INPUT;
-      } else {
-        d4 L0 = to_local(F, P0), L1 = to_local(F, P1), L2 = to_local(F, P2), L3 = to_local(F, P3);
-        Hodo hc;
-        hc.L0 = to_f4(L0);
-        hc.D0 = to_f4(sub4(L1, L0));
-        hc.D1 = to_f4(sub4(L2, L1));
-        hc.D2 = to_f4(sub4(L3, L2));
-        Delta cur;  // conversion {p0,p1,p2,p3} -> {p,d,t0,t1} (3.1 P:372-375)
-        cur.p = hc.L0;
-        cur.d = to_f4(sub4(L3, L0));
-        cur.t0 = hc.D0;
-        cur.t1 = hc.D2;
-        // ray interval [0, tmax) in local distance units s = t |d| - ts
-        const float lo0 = (float)(-F.ts);
-        const float hi0 = (float)((double)ray0.w * F.lw - F.ts);
-        float tmin, tmax;
-        uint32_t tag;
-        slab(cur, lo0, hi0, true, true, tmin, tmax, tag);
-        uint32_t bits = 0, size = 1u << FIBER_MAX_DEPTH, start = 0;
-        uint32_t tests = 0, backtracks = 0;
-        bool found = false;
-        float c0 = 0.0f, c1 = 0.0f;
-        // ---- a3-a6: the stackless loop
-        while (true) {
-          ++tests;
-          bool pass = cylinder(cur, c0, c1);
-          // pruning test P:1618 with F1 (empty interval) and F5 (explicit miss)
-          pass = pass && (c1 >= tmin) && (c0 <= tmax) && (tmin <= tmax);
-          if (pass) {
-            if (size <= min_size) {  // leaf: first hit terminates
-              found = true;
-              break;
-            }
-            bool right, both;
-            descend(cur, c0, c1, tmin, tmax, tag, right, both);
-            // go_down (lst:bitstring_manipulation P:1516-1528)
-            size >>= 1;
-            if (both) bits |= size;
-            if (right) start |= size;
-          } else {
-            if (bits == 0u) break;  // done
-            ++backtracks;
-            // jump_up: ctz of the pending bit string
-            size = bits & (0u - bits);
-            start ^= size;
-            bits ^= size;
-            start &= ~(size - 1u);
-            float u0, u1;
-            get_interval(start, size, u0, u1);
-            recompute(hc, u0, u1, cur);
-            slab(cur, lo0, hi0, start == 0u, start + size == (1u << FIBER_MAX_DEPTH), tmin, tmax,
-                 tag);
-          }
-        }
-        if (found) {
-          // F2: entry into the cropped cylinder; F6: kind from the binding constraint
-          float sstar = fmaxf(c0, tmin);
-          uint32_t kind = FIBER_KIND_LATERAL;
-          bool inside = false;
-          if (!(c0 >= tmin)) {
-            if (tag == TAG_ORIGIN) inside = true;
-            else if (tag == TAG_START && start == 0u) kind = FIBER_KIND_CAP0;
-            else if (tag == TAG_END && start + size == (1u << FIBER_MAX_DEPTH)) kind = FIBER_KIND_CAP1;
-            else kind = FIBER_KIND_WEDGE;
-          }
-          bool hit = sstar < tmax;
-          if (inside) {
-            kind = FIBER_KIND_WEDGE;  // finalise like a crop-plane entry at s = -ts
-            sstar = lo0;
-          }
-          if (hit) {
-            finalize(ray0, ray1, P0, P1, P2, P3, start, depth, kind, sstar, t_out, u_out, n_out, hit);
-            if (inside) {
-              t_out = hit ? 0.0f : t_out;
-              kind = FIBER_KIND_LATERAL;
-            }
-          }
-          if (hit) flags |= FIBER_HIT | (kind << FIBER_KIND_SHIFT) | (inside ? FIBER_INSIDE : 0u);
-        }
-        flags |= (min(backtracks, 255u) << 8) | (min(tests, 65535u) << 16);
-      }
-    }
-    if (hits) hits[i] = make_float4(t_out, u_out, __uint_as_float(n_out), __uint_as_float(flags));
-    if (kNearest && (flags & FIBER_HIT)) {
-      unsigned long long key =
-          ((unsigned long long)__float_as_uint(t_out) << 32) | (unsigned long long)(uint32_t)i;
-      atomicMin(&nearest[pr.x], key);
+// The frame origin o' = o + ts w is placed on the ray next to the segment anchor
+// c = fl((P0 + P3) / 2).  Local coordinates of a point X are (<X-o', b1>, <X-o', b2>,
+// <X-o', w>) with (b1, b2) the FP32 Duff/Frisvad basis of w.  They are split as
+// <X - c, b> (small, FP32) + rho, rho = <c - o - ts w, b>: rho carries the cancellation of
+// |c - o| ~ |ray length| and is formed in FP64 from the exact FP32 inputs, so every local
+// coordinate is accurate to FP32 rounding of the SEGMENT's size.  The ray is then the unit
+// ray (0,0,0) + z (0,0,1) of P:475-481 with z = (t - ts) |w|^2.
+struct Setup32 {
+  float4 b1, b2;  // xyz used
+  float ts, iww;
+};
+
+__device__ __forceinline__ bool frame32(const float4 ray0, const float4 ray1, const float4 P0,
+                                        const float4 P3, Setup32& S, float4& rho, float4& c) {
+  const float4 w = ray1;
+  float ww = fmaf(w.x, w.x, fmaf(w.y, w.y, w.z * w.z));
+  bool ok = isfinite(ray0.x) && isfinite(ray0.y) && isfinite(ray0.z) && isfinite(w.x) &&
+            isfinite(w.y) && isfinite(w.z) && !(ray0.w <= 0.0f) && !isnan(ray0.w) && ww > 0.0f;
+  float sign = copysignf(1.0f, w.z);
+  float a = -1.0f / (sign + w.z);
+  float b = w.x * w.y * a;
+  S.b1 = make_float4(fmaf(sign * w.x * w.x, a, 1.0f), sign * b, -sign * w.x, 0.0f);
+  S.b2 = make_float4(b, fmaf(w.y * w.y, a, sign), -w.y, 0.0f);
+  c = make_float4(0.5f * (P0.x + P3.x), 0.5f * (P0.y + P3.y), 0.5f * (P0.z + P3.z), 0.0f);
+  S.iww = 1.0f / ww;
+  S.ts = fmaf(c.x - ray0.x, w.x, fmaf(c.y - ray0.y, w.y, (c.z - ray0.z) * w.z)) * S.iww;
+  // FP64: v = c - o - ts w (exact inputs), rho = (<v,b1>, <v,b2>, <v,w>)
+  double ts = S.ts;
+  double vx = fma(-ts, (double)w.x, (double)c.x - (double)ray0.x);
+  double vy = fma(-ts, (double)w.y, (double)c.y - (double)ray0.y);
+  double vz = fma(-ts, (double)w.z, (double)c.z - (double)ray0.z);
+  rho = make_float4((float)fma(vx, (double)S.b1.x, fma(vy, (double)S.b1.y, vz * (double)S.b1.z)),
+                    (float)fma(vx, (double)S.b2.x, fma(vy, (double)S.b2.y, vz * (double)S.b2.z)),
+                    (float)fma(vx, (double)w.x, fma(vy, (double)w.y, vz * (double)w.z)), 0.0f);
+  return ok;
+}
+
+// ------------------------------------------------------------------------------------
+// kernel parameters and record helpers
+// ------------------------------------------------------------------------------------
+struct Params {
+  const float4* rays;
+  int64_t n_rays;
+  const float4 *p0, *p1, *p2, *p3;
+  const uint32_t* sflags;
+  int64_t n_segs;
+  const uint2* pairs;
+  uint32_t n_pairs;
+  int depth;
+  uint32_t min_size;  // 2^(23 - depth), lst:algorithm
+  float4* hits;
+  unsigned long long* nearest;
+  unsigned int* counter;  // slot: [0] K2 pair counter, [1] K3 chunk counter,
+                          // [2] K2 blocks done, [3] K3 blocks done (all zero at launch)
+#ifdef FIBER_TRACE
+  uint32_t trace_pair;  // test build only: per-iteration records of one pair
+  float4* trace;        // [kTraceCap] x 3 float4
+#endif
+};
+#ifdef FIBER_TRACE
+constexpr int kTraceCap = 256;
+__device__ unsigned int g_trace_n;
+#endif
+
+// Internal flag of a provisional record (never visible after fiber_intersect returns).
+constexpr uint32_t kProvisional = 1u << 6;
+
+__device__ __forceinline__ void write_record(const Params& p, uint32_t i, uint32_t ray, float t,
+                                             float u, uint32_t n_oct, uint32_t flags) {
+  if (p.hits) p.hits[i] = make_float4(t, u, __uint_as_float(n_oct), __uint_as_float(flags));
+  if (p.nearest && (flags & FIBER_HIT)) {
+    unsigned long long key =
+        ((unsigned long long)__float_as_uint(t) << 32) | (unsigned long long)i;
+    atomicMin(&p.nearest[ray], key);
+  }
+}
+
+// world vector v (xyz, w = radius part) -> local frame (no translation)
+__device__ __forceinline__ float4 rot(const Setup32& S, const float4 w, float4 v) {
+  return make_float4(dot3(v, S.b1), dot3(v, S.b2), dot3(v, w), v.w);
+}
+
+// ------------------------------------------------------------------------------------
+// per-pair traversal state and one iteration of the loop
+// ------------------------------------------------------------------------------------
+struct Lane {
+  Delta cur;
+  float tmin, tmax, lo0, hi0, c0;
+  float stmin, stmax;  // interval saved at level kCropLevel (deep backtracks)
+  uint32_t tag, stag, bits, start, size, tests, backtracks;
+  uint32_t ncache, cache_top, cache_right;  // parent-cache fill, ring top, near-side bits
+};
+
+enum : int { ST_RUNNING = 0, ST_MISS = 1, ST_HIT = 2, ST_NEED_BT = 3 };
+
+// Per-lane shared-memory slots, component-major (stride kThreads: conflict-free): the
+// ray-frame curve for re-calculation, and a ring of kFarCache parents of pending levels
+// (the far child is rebuilt from its parent on backtracking, so a push is 4 plain stores).
+struct HodoRef {
+  float4* base;  // hodograph slot: &smem[threadIdx.x]
+  float4* far;   // parent ring:    &smem[4 * kThreads + threadIdx.x]
+  __device__ __forceinline__ void push(const Delta& f, uint32_t slot) const {
+    float4* q = far + slot * 4 * kThreads;
+    q[0] = f.p;
+    q[kThreads] = f.d;
+    q[2 * kThreads] = f.t0;
+    q[3 * kThreads] = f.t1;
+  }
+  __device__ __forceinline__ void pop(Delta& f, uint32_t slot) const {
+    const float4* q = far + slot * 4 * kThreads;
+    f.p = q[0];
+    f.d = q[kThreads];
+    f.t0 = q[2 * kThreads];
+    f.t1 = q[3 * kThreads];
+  }
+  __device__ __forceinline__ void store(const Hodo& h) const {
+    base[0] = h.L0;
+    base[kThreads] = h.D0;
+    base[2 * kThreads] = h.D1;
+    base[3 * kThreads] = h.D2;
+  }
+  __device__ __forceinline__ Hodo load() const {
+    Hodo h;
+    h.L0 = base[0];
+    h.D0 = base[kThreads];
+    h.D1 = base[2 * kThreads];
+    h.D2 = base[3 * kThreads];
+    return h;
+  }
+};
+
+// One prepared pair: the ray-frame curve, the ray interval and the root slab.
+struct Prepared {
+  Hodo h;
+  float lo0, hi0, tmin, tmax;
+  uint32_t pair, badseg, tag;
+};
+
+// a2: transform pair i's segment into its ray frame (lst:transform_curve P:1482-1512) and
+// form the root interval.  Returns false for bad input (written as a miss).
+__device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e) {
+  const uint2 pr = __ldg(&p.pairs[i]);
+  if ((int64_t)pr.x >= p.n_rays || (int64_t)pr.y >= p.n_segs) {
+    write_record(p, i, 0, INFINITY, 0.0f, 0u, FIBER_BAD_INPUT);
+    return false;
+  }
+  const float4 ray0 = __ldg(&p.rays[2 * (int64_t)pr.x]);
+  const float4 ray1 = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
+  const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
+  const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
+  e.badseg = __ldg(&p.sflags[pr.y]) != 0u ? FIBER_BAD_SEGMENT : 0u;
+  e.pair = i;
+  Setup32 S;
+  float4 rho, c;
+  if (!frame32(ray0, ray1, P0, P3, S, rho, c)) {
+    write_record(p, i, pr.x, INFINITY, 0.0f, 0u, FIBER_BAD_INPUT | e.badseg);
+    return false;
+  }
+  const float4 w = ray1;
+  // differences are rotated directly, so they keep the relative precision of the inputs
+  e.h.L0 = rot(S, w, P0 - c) + rho;
+  e.h.L0.w = P0.w;
+  e.h.D0 = rot(S, w, P1 - P0);
+  e.h.D1 = rot(S, w, P2 - P1);
+  e.h.D2 = rot(S, w, P3 - P2);
+  // ray interval [0, tmax) in local z units: z = (t - ts) |w|^2
+  float ww = 1.0f / S.iww;
+  e.lo0 = -S.ts * ww;
+  e.hi0 = (ray0.w - S.ts) * ww;
+  Delta cur;  // conversion {p0,p1,p2,p3} -> {p,d,t0,t1} (3.1 P:372-375)
+  cur.p = e.h.L0;
+  cur.d = e.h.D0 + e.h.D1 + e.h.D2;
+  cur.t0 = e.h.D0;
+  cur.t1 = e.h.D2;
+  slab(cur, e.lo0, e.hi0, true, true, e.tmin, e.tmax, e.tag);
+  return true;
+}
+
+// One iteration: node test, then descend.  Returns ST_RUNNING, ST_MISS, ST_HIT (leaf
+// accepted; L.c0 holds the cylinder entry) or ST_NEED_BT (pruned with levels pending).
+__device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
+                                    float4* trace = nullptr) {
+  ++L.tests;
+  float c0, c1;
+  bool pass = cylinder(L.cur, c0, c1);
+  // pruning test P:1618 with F1 (empty interval) and F5 (explicit miss)
+  pass = pass && (c1 >= L.tmin) && (c0 <= L.tmax) && (L.tmin <= L.tmax);
+#ifdef FIBER_TRACE
+  if (trace) {
+    unsigned k = atomicAdd(&g_trace_n, 1u);
+    if (k < kTraceCap) {
+      trace[3 * k] = make_float4(__uint_as_float(L.start), __uint_as_float(L.size),
+                                 __uint_as_float(L.bits), __uint_as_float(pass ? 1u : 0u));
+      trace[3 * k + 1] = make_float4(c0, c1, L.tmin, L.tmax);
+      trace[3 * k + 2] = make_float4(__uint_as_float(L.tag), __uint_as_float(L.ncache), 0.0f, 0.0f);
     }
   }
+#endif
+  if (!pass) return L.bits == 0u ? ST_MISS : ST_NEED_BT;  // done / backtrack
+  if (L.size <= min_size) {  // leaf: first hit terminates
+    L.c0 = c0;
+    return ST_HIT;
+  }
+  Split sp = partition(L.cur, c0, c1, L.tmin, L.tmax, L.tag, L.size > kCropMinSize);
+  // go_down (lst:bitstring_manipulation P:1516-1528)
+  L.size >>= 1;
+  if (sp.both) {
+    // remember the parent: the next jump_up returns to the deepest pending level, i.e.
+    // the most recent push (LIFO); the ring drops the oldest entry when full
+    L.bits |= L.size;
+    L.cache_top = (L.cache_top + 1u) % kFarCache;
+    hs.push(L.cur, L.cache_top);
+    L.cache_right = sp.right ? (L.cache_right | (1u << L.cache_top))
+                             : (L.cache_right & ~(1u << L.cache_top));
+    L.ncache = min(L.ncache + 1u, (uint32_t)kFarCache);
+  }
+  if (sp.right) L.start |= L.size;
+  child(L.cur, sp, sp.right, L.cur);
+  if (L.size == kCropMinSize) {
+    L.stmin = L.tmin;
+    L.stmax = L.tmax;
+    L.stag = L.tag;
+  }
+  return ST_RUNNING;
+}
+
+// jump_up to the deepest pending level, the far node's curve (rebuilt from
+// the cached parent, else re-calculated) and its own interval (F7).
+__device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
+  ++L.backtracks;
+  L.size = L.bits & (0u - L.bits);  // lowest pending bit (ctz)
+  L.start ^= L.size;
+  L.bits ^= L.size;
+  L.start &= ~(L.size - 1u);
+  const bool cached = L.ncache > 0u;
+  if (cached) {
+    Delta parent;
+    hs.pop(parent, L.cache_top);
+    const bool near_right = (L.cache_right >> L.cache_top) & 1u;
+    Split sp;
+    split_geometry(parent, sp);
+    child(parent, sp, !near_right, L.cur);
+    L.cache_top = (L.cache_top + kFarCache - 1u) % kFarCache;
+    --L.ncache;
+  } else {
+    float u0, u1;
+    get_interval(L.start, L.size, u0, u1);
+    recompute(hs.load(), u0, u1, L.cur);  // lst:recalculation P:1371-1385
+  }
+  if (L.size >= kCropMinSize) {
+    slab(L.cur, L.lo0, L.hi0, L.start == 0u, L.start + L.size == (1u << FIBER_MAX_DEPTH), L.tmin,
+         L.tmax, L.tag, !cached);
+    if (L.size == kCropMinSize) {
+      L.stmin = L.tmin;
+      L.stmax = L.tmax;
+      L.stag = L.tag;
+    }
+  } else {
+    L.tmin = L.stmin;
+    L.tmax = L.stmax;
+    L.tag = L.stag;
+  }
+}
+
+__device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
+  return (min(L.backtracks, 255u) << 8) | (min(L.tests, 65535u) << 16);
+}
+
+// Pair ended with status st: write the miss, or the provisional hit record for K3
+// (z* bits, start | kind << 24 | inside << 26, 0, counters | bad_segment | kProvisional).
+__device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane& L, int st,
+                                         uint32_t badseg) {
+  if (st == ST_HIT) {
+    // F2: entry into the cropped cylinder; F6: kind from the binding constraint
+    float zs = fmaxf(L.c0, L.tmin);
+    uint32_t kind = FIBER_KIND_LATERAL, inside = 0;
+    if (!(L.c0 >= L.tmin)) {
+      if (L.tag == TAG_ORIGIN) inside = 1, kind = FIBER_KIND_WEDGE;
+      else if (L.tag == TAG_START && L.start == 0u) kind = FIBER_KIND_CAP0;
+      else if (L.tag == TAG_END && L.start + L.size == (1u << FIBER_MAX_DEPTH)) kind = FIBER_KIND_CAP1;
+      else kind = FIBER_KIND_WEDGE;
+    }
+    if (zs < L.hi0) {  // strictly before the RAY's t_max
+      p.hits[i] = make_float4(zs, __uint_as_float(L.start | (kind << 24) | (inside << 26)), 0.0f,
+                              __uint_as_float(counter_bits(L) | badseg | kProvisional));
+      return;
+    }
+  }
+  p.hits[i] = make_float4(INFINITY, 0.0f, 0.0f, __uint_as_float(badseg | counter_bits(L)));
+}
+
+// a7 for one provisional hit (all lanes of the batch run it together, converged).
+__device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
+  const float4 rec = p.hits[i];
+  const uint2 pr = __ldg(&p.pairs[i]);
+  const float4 ray0 = __ldg(&p.rays[2 * (int64_t)pr.x]);
+  const float4 ray1 = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
+  const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
+  const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
+  const uint32_t y = __float_as_uint(rec.y);
+  uint32_t start = y & 0x00ffffffu, kind = (y >> 24) & 3u;
+  bool inside = (y >> 26) & 1u;
+  uint32_t flags = __float_as_uint(rec.w) & ~kProvisional;
+  // the FP32 z* as a ray parameter (only used for WEDGE / INSIDE entries)
+  Setup32 S;
+  float4 rho, c;
+  frame32(ray0, ray1, P0, P3, S, rho, c);
+  float t32 = fmaf(rec.x, S.iww, S.ts);
+  float t, u;
+  uint32_t n_oct;
+  bool hit;
+  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, t32, t, u, n_oct, hit);
+  if (inside && hit) {
+    t = 0.0f;
+    kind = FIBER_KIND_LATERAL;
+  }
+  if (hit) flags |= FIBER_HIT | (kind << FIBER_KIND_SHIFT) | (inside ? FIBER_INSIDE : 0u);
+  write_record(p, i, pr.x, t, u, n_oct, flags);
+}
+
+// The last block of a kernel to finish returns its counter slot to zero (all blocks have
+// stopped taking work by then), so the slot is ready for a later call without a memset.
+__device__ __forceinline__ void release_counter(unsigned int* slot, int work, int done) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&slot[done], 1u) == gridDim.x - 1u) {
+      atomicExch(&slot[work], 0u);
+      atomicExch(&slot[done], 0u);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K2, the traversal kernel: persistent warps whose lanes are refilled in epochs
+// (DESIGN.md "Kernel").  Every kEpoch iterations the warp votes; once at least kRefill
+// lanes are idle they all take new pairs from one atomicAdd and run setup together, so
+// setup and the loop both execute with most lanes active.  A pair runs from setup to its
+// end in one lane without interruption, so its result is a deterministic function of the
+// pair alone (independent of the launch shape and of the schedule).  Hits leave
+// provisional records that K3 finalises.
+// ------------------------------------------------------------------------------------
+constexpr int kEpoch = 2;
+constexpr uint32_t kRefill = 16;
+
+__device__ __forceinline__ void start_lane(const Prepared& e, Lane& L, HodoRef hs) {
+  hs.store(e.h);
+  L.cur.p = e.h.L0;
+  L.cur.d = e.h.D0 + e.h.D1 + e.h.D2;
+  L.cur.t0 = e.h.D0;
+  L.cur.t1 = e.h.D2;
+  L.lo0 = e.lo0;
+  L.hi0 = e.hi0;
+  L.tmin = L.stmin = e.tmin;
+  L.tmax = L.stmax = e.tmax;
+  L.tag = L.stag = e.tag;
+  L.bits = 0;
+  L.size = 1u << FIBER_MAX_DEPTH;
+  L.start = 0;
+  L.tests = 0;
+  L.backtracks = 0;
+  L.c0 = 0.0f;
+  L.ncache = 0;
+  L.cache_top = 0;
+  L.cache_right = 0;
+}
+
+__global__ void __launch_bounds__(kThreads, 3) intersect_kernel(const Params p) {
+  extern __shared__ float4 smem[];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  HodoRef hs{&smem[threadIdx.x], &smem[4 * kThreads + threadIdx.x]};
+  const uint32_t min_size = p.min_size;
+  Lane L;
+  uint32_t pair = 0, badseg = 0;
+  bool active = false, drained = false;
+  while (true) {
+    const unsigned idle = __ballot_sync(0xffffffffu, !active);
+    if (!drained && (__popc(idle) >= (int)kRefill || idle == 0xffffffffu)) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&p.counter[0], (uint32_t)__popc(idle));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + (uint32_t)__popc(idle) >= p.n_pairs) drained = true;
+      if (!active) {
+        const uint32_t i = base + __popc(idle & lt);
+        if (i < p.n_pairs) {
+          Prepared e;
+          if (prepare(p, i, e)) {  // a2
+            start_lane(e, L, hs);
+            pair = e.pair;
+            badseg = e.badseg;
+            active = true;
+          }
+        }
+      }
+    }
+    if (__ballot_sync(0xffffffffu, active) == 0u) {
+      if (drained) break;
+      continue;
+    }
+#pragma unroll 1
+    for (int k = 0; k < kEpoch; ++k) {
+      if (active) {
+#ifdef FIBER_TRACE
+        const int st = step(L, hs, min_size, pair == p.trace_pair ? p.trace : nullptr);
+#else
+        const int st = step(L, hs, min_size);  // a3-a4
+#endif
+        if (st == ST_NEED_BT) {
+          backtrack(L, hs);  // a5
+        } else if (st != ST_RUNNING) {
+          end_pair(p, pair, L, st, badseg);  // a6
+          active = false;
+        }
+      }
+    }
+  }
+  release_counter(p.counter, 0, 2);
+}
+
+// ------------------------------------------------------------------------------------
+// K3, the finalisation kernel: scans the records, queues provisional hits per warp and
+// finalises them in FP64 32 at a time (converged).  a7, lst:calc_intersection P:1546-1587.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 2) finalize_kernel(const Params p) {
+  __shared__ uint32_t s_q[kWarps][kQueue];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t nq = 0;
+  auto flush = [&](uint32_t take) {
+    if (lane < take) finalize_one(p, s_q[wid][lane]);
+    __syncwarp();
+    uint32_t mv = 0;
+    bool has = lane + take < nq;
+    if (has) mv = s_q[wid][lane + take];
+    __syncwarp();
+    if (has) s_q[wid][lane] = mv;
+    nq -= take;
+    __syncwarp();
+  };
+  while (true) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&p.counter[1], 128u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= p.n_pairs) break;
+    for (uint32_t k = 0; k < 128u; k += 32u) {
+      const uint32_t i = base + k + lane;
+      bool prov = false;
+      if (i < p.n_pairs) prov = (__float_as_uint(p.hits[i].w) & kProvisional) != 0u;
+      unsigned m = __ballot_sync(0xffffffffu, prov);
+      if (prov) s_q[wid][nq + __popc(m & lt)] = i;
+      nq += __popc(m);
+      __syncwarp();
+      if (nq >= 32u) flush(32u);
+    }
+  }
+  while (nq > 0u) flush(min(nq, 32u));
+  release_counter(p.counter, 1, 3);
 }
 
 __global__ void fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
@@ -268,11 +640,52 @@ __global__ void fill_u64(unsigned long long* p, int64_t n, unsigned long long v)
 
 using namespace fiberx;
 
+// Per-device launch constants, queried once per process and device (immutable afterwards;
+// a call otherwise spends far longer in these queries than the GPU spends on 1M pairs).
+struct LaunchInfo {
+  int sms, k2_per_sm, k3_per_sm;
+  unsigned int* slots;  // kSlots x 4 work counters, zero between uses
+};
+constexpr int kSlots = 1024;  // calls in flight on one device at a time (any streams)
+static std::atomic<unsigned> g_next_slot{0};
+
+static const LaunchInfo* launch_info() {
+  static std::mutex mu;
+  static LaunchInfo info[64];
+  static bool ready[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ready[dev]) {
+    LaunchInfo li{};
+    cudaDeviceGetAttribute(&li.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(intersect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k2_per_sm, intersect_kernel, kThreads,
+                                                  kSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k3_per_sm, finalize_kernel, kThreads, 0);
+    if (li.k2_per_sm < 1) li.k2_per_sm = 1;
+    if (li.k3_per_sm < 1) li.k3_per_sm = 1;
+    if (cudaMalloc((void**)&li.slots, kSlots * 4 * sizeof(unsigned int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(li.slots, 0, kSlots * 4 * sizeof(unsigned int)) != cudaSuccess) return nullptr;
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    if (cudaGetLastError() != cudaSuccess || li.sms < 1) return nullptr;
+    info[dev] = li;
+    ready[dev] = true;
+  }
+  return &info[dev];
+}
+
+#ifdef FIBER_TRACE
+static uint32_t g_trace_pair = 0xffffffffu;
+static float4* g_trace_buf = nullptr;
+#endif
+
 static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                             const fiber_pair* pairs, int64_t n_pairs, int max_depth,
                             fiber_hit* hits, uint64_t* nearest, void* stream) {
   if (n_rays < 0 || n_pairs < 0 || n_rays >= ((int64_t)1 << 32) ||
-      n_pairs >= ((int64_t)1 << 32) || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
+      n_pairs >= ((int64_t)1 << 32) - 64 || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
     return set_error(FIBER_EINVAL, "fiber_intersect: bad size or depth");
   if (n_pairs > 0 && (!rays || !pairs || (!hits && !nearest) || !segs->p0 || !segs->p1 ||
                       !segs->p2 || !segs->p3 || !segs->flags))
@@ -281,25 +694,69 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   if (rc != FIBER_OK) return rc;
   if (n_pairs == 0) return FIBER_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t blocks = (n_pairs + 255) / 256;
-  int64_t cap = (int64_t)sms * 8;
-  if (blocks > cap) blocks = cap;
-  if (nearest) {
-    intersect_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(
-        (const float4*)rays, n_rays, (const float4*)segs->p0, (const float4*)segs->p1,
-        (const float4*)segs->p2, (const float4*)segs->p3, segs->flags, segs->n,
-        (const uint2*)pairs, n_pairs, max_depth, (float4*)hits, (unsigned long long*)nearest);
-  } else {
-    intersect_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(
-        (const float4*)rays, n_rays, (const float4*)segs->p0, (const float4*)segs->p1,
-        (const float4*)segs->p2, (const float4*)segs->p3, segs->flags, segs->n,
-        (const uint2*)pairs, n_pairs, max_depth, (float4*)hits, nullptr);
+  const LaunchInfo* li = launch_info();
+  if (!li) return set_error(FIBER_ECUDA, "fiber_intersect: device query failed");
+  int64_t chunks = (n_pairs + 31) / 32;
+  int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
+  if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
+  // work counters: a self-resetting slot of the per-device pool (no per-call allocation);
+  // scratch records only when the caller passes no hits buffer (nearest-only calls)
+  unsigned int* counter = li->slots + 4 * (g_next_slot.fetch_add(1u) % kSlots);
+  void* scratch = nullptr;
+  if (!hits) {
+    cudaError_t e = cudaMallocAsync(&scratch, (size_t)n_pairs * sizeof(fiber_hit), st);
+    if (e != cudaSuccess) {
+      char buf[300];
+      snprintf(buf, sizeof(buf), "fiber_intersect: scratch: %s", cudaGetErrorString(e));
+      return set_error(FIBER_ECUDA, buf);
+    }
+    hits = (fiber_hit*)scratch;
   }
-  return check_launch("fiber_intersect");
+  Params p;
+  p.rays = (const float4*)rays;
+  p.n_rays = n_rays;
+  p.p0 = (const float4*)segs->p0;
+  p.p1 = (const float4*)segs->p1;
+  p.p2 = (const float4*)segs->p2;
+  p.p3 = (const float4*)segs->p3;
+  p.sflags = segs->flags;
+  p.n_segs = segs->n;
+  p.pairs = (const uint2*)pairs;
+  p.n_pairs = (uint32_t)n_pairs;
+  p.depth = max_depth;
+  p.min_size = 1u << (FIBER_MAX_DEPTH - max_depth);
+#ifdef FIBER_TRACE
+  p.trace_pair = g_trace_pair;
+  p.trace = g_trace_buf;
+#endif
+  p.hits = (float4*)hits;
+  p.nearest = nullptr;  // hits only come out of K3
+  p.counter = counter;
+  intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
+  rc = check_launch("fiber_intersect");
+  if (rc == FIBER_OK) {
+    int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
+    int64_t fchunks = (n_pairs + 127) / 128;
+    if (fblocks * kWarps > fchunks) fblocks = (fchunks + kWarps - 1) / kWarps;
+    p.nearest = (unsigned long long*)nearest;
+    finalize_kernel<<<(unsigned)fblocks, kThreads, 0, st>>>(p);
+    rc = check_launch("fiber_intersect (finalize)");
+  }
+  if (scratch) cudaFreeAsync(scratch, st);
+  return rc;
 }
+
+#ifdef FIBER_TRACE
+// Test build only: record the iterations of pair `pair` into trace (device float4[3*256]);
+// returns nothing; the next fiber_intersect call fills it.  g_trace_n counts records.
+extern "C" int fiber_debug_trace(uint32_t pair, void* trace) {
+  g_trace_pair = pair;
+  g_trace_buf = (float4*)trace;
+  unsigned zero = 0;
+  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
+  return FIBER_OK;
+}
+#endif
 
 extern "C" int fiber_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                                const fiber_pair* pairs, int64_t n_pairs, int max_depth,

@@ -14,6 +14,9 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfiber.so")
+# test hook: FIBER_LIB_VARIANT=ieee loads the IEEE-math test build libfiber_ieee.so
+if os.environ.get("FIBER_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, f"libfiber_{os.environ['FIBER_LIB_VARIANT']}.so")
 
 FIBER_OK, FIBER_EINVAL, FIBER_ECUDA, FIBER_EDEVICE = 0, -1, -2, -3
 MAX_DEPTH = 23

@@ -39,8 +39,13 @@ def compare(g: dict, o: dict) -> dict:
         t_rel = np.where(cmp, np.abs(g["t"] - o["t"]) / np.maximum(np.abs(o["t"]), 1e-30), 0)
         u_abs = np.where(cmp, np.abs(g["u"] - o["u"]), 0)
         ang = np.where(cmp, _angle(g["n"], o["n"]), 0)
-    kind_mis = cmp & ((g["kind"] != oracle_kind_to_gpu(o["kind"])) |
-                      (g["inside"] != (o["kind"] == 4)))
+    # CAP kinds fix u = 0/1 and the cap normal; LATERAL and WEDGE share the listing's
+    # normal formula and differ only by which side of a leaf boundary the
+    # entry point is assigned to, so they form one class here
+    gk, ok_ = g["kind"], oracle_kind_to_gpu(o["kind"])
+    gcap = (gk == 1) | (gk == 2)
+    ocap = (ok_ == 1) | (ok_ == 2)
+    kind_mis = cmp & ((gcap != ocap) | (gcap & (gk != ok_)) | (g["inside"] != (o["kind"] == 4)))
     bad = cmp & ((t_rel > TOL_T) | (u_abs > TOL_U) | (ang > TOL_N) | kind_mis)
     return {
         "n": n, "hits": int(o["hit"].sum()), "grazing": int(grazing.sum()),
