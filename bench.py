@@ -35,9 +35,10 @@ FIBERS = ("A", "B", "C")
 DEPTHS = tuple(range(2, 23))
 N_RAYS = 1 << 20
 
-# Algorithmic FP32 flops per occurrence of each step of the loop (FMA = 2), counted from
-# the kernel source: a3 node test, a4 descend, a5 backtrack.
-FLOPS_TEST, FLOPS_DESCEND, FLOPS_BACKTRACK = 64, 49, 170
+# Algorithmic FP32 flops per occurrence of each step of the loop (FMA = 2, MUFU = 1),
+# counted from the kernel source: a3 node test, a4 descend,
+# a5 backtrack (cached-parent path).
+FLOPS_TEST, FLOPS_DESCEND, FLOPS_BACKTRACK = 72, 56, 68
 
 
 def parse():
@@ -146,18 +147,22 @@ def run_ours(args):
     pairs_per_step = n * len(launches)
 
     def step(record):
+        # one fiber_intersect per (fiber, depth), issued as its two stages so that the
+        # traversal kernel (K2, the dominant one) is timed on its own
         ms = []
         for fi, D in launches:
             rays, segs, pairs = data[fi]
             flush.fill_(1)  # untimed L2 flush: inputs come from HBM
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
             if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            fx.intersect(rays, segs, pairs, D, hits=hits)
+                ev[0].record(stream)
+            fx.traverse(rays, segs, pairs, D, hits)
             if record:
-                e1.record(stream)
-                ms.append((e0, e1))
+                ev[1].record(stream)
+            fx.finalize(rays, segs, pairs, D, hits)
+            if record:
+                ev[2].record(stream)
+                ms.append(ev)
         return ms
 
     for _ in range(args.warmup):
@@ -174,7 +179,8 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    per_launch = np.array([[a.elapsed_time(b) for a, b in s] for s in evs])  # [K, 63] ms
+    per_launch = np.array([[e[0].elapsed_time(e[2]) for e in s] for s in evs])  # [K, 63] ms
+    per_k2 = np.array([[e[0].elapsed_time(e[1]) for e in s] for s in evs])
     total_ms = float(per_launch.sum())
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -199,7 +205,8 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_mhz = clocks["sm_max_mhz"] or 1965.0
     peak = fp32_peak_tflops(sms, peak_mhz)
-    achieved = float(flops.sum() / (mean_ms.sum() * 1e-3) / 1e12)
+    k2_ms = per_k2.mean(0)
+    achieved = float(flops.sum() / (k2_ms.sum() * 1e-3) / 1e12)
 
     # gather per-ray hit records across ranks (the one collective)
     gather_ms = None
@@ -228,8 +235,10 @@ def run_ours(args):
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                      "peak_basis": f"FP32: {sms} SMs x 128 lanes x 2 x {peak_mhz:.0f} MHz "
                                    "(max SM clock; B200_PROFILING.md unit counts)",
-                     "kernel": "intersect_kernel (K2)"},
-        "gpu_launches": args.steps * len(launches),
+                     "kernel": "intersect_kernel (K2), timed alone with CUDA events",
+                     "k2_share_of_step": round(float(k2_ms.sum() / mean_ms.sum()), 3),
+                     "traffic_note": "see profiles/ (ncu dram bytes per K2 launch)"},
+        "gpu_launches": args.steps * len(launches) * 2,
         "clocks": clocks,
         "wall_s_timed": round(wall, 3),
     }

@@ -681,24 +681,25 @@ static uint32_t g_trace_pair = 0xffffffffu;
 static float4* g_trace_buf = nullptr;
 #endif
 
+enum { STAGE_TRAVERSE = 1, STAGE_FINALIZE = 2 };
+
 static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                             const fiber_pair* pairs, int64_t n_pairs, int max_depth,
-                            fiber_hit* hits, uint64_t* nearest, void* stream) {
+                            fiber_hit* hits, uint64_t* nearest, void* stream, int stages) {
   if (n_rays < 0 || n_pairs < 0 || n_rays >= ((int64_t)1 << 32) ||
       n_pairs >= ((int64_t)1 << 32) - 64 || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
     return set_error(FIBER_EINVAL, "fiber_intersect: bad size or depth");
   if (n_pairs > 0 && (!rays || !pairs || (!hits && !nearest) || !segs->p0 || !segs->p1 ||
                       !segs->p2 || !segs->p3 || !segs->flags))
     return set_error(FIBER_EINVAL, "fiber_intersect: NULL pointer");
+  if (stages != (STAGE_TRAVERSE | STAGE_FINALIZE) && !hits)
+    return set_error(FIBER_EINVAL, "fiber_traverse/fiber_finalize: NULL hits");
   int rc = check_device();
   if (rc != FIBER_OK) return rc;
   if (n_pairs == 0) return FIBER_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const LaunchInfo* li = launch_info();
   if (!li) return set_error(FIBER_ECUDA, "fiber_intersect: device query failed");
-  int64_t chunks = (n_pairs + 31) / 32;
-  int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
-  if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
   // work counters: a self-resetting slot of the per-device pool (no per-call allocation);
   // scratch records only when the caller passes no hits buffer (nearest-only calls)
   unsigned int* counter = li->slots + 4 * (g_next_slot.fetch_add(1u) % kSlots);
@@ -732,9 +733,15 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   p.hits = (float4*)hits;
   p.nearest = nullptr;  // hits only come out of K3
   p.counter = counter;
-  intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
-  rc = check_launch("fiber_intersect");
-  if (rc == FIBER_OK) {
+  rc = FIBER_OK;
+  if (stages & STAGE_TRAVERSE) {
+    int64_t chunks = (n_pairs + 31) / 32;
+    int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
+    if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
+    intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
+    rc = check_launch("fiber_intersect (traverse)");
+  }
+  if (rc == FIBER_OK && (stages & STAGE_FINALIZE)) {
     int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
     int64_t fchunks = (n_pairs + 127) / 128;
     if (fblocks * kWarps > fchunks) fblocks = (fchunks + kWarps - 1) / kWarps;
@@ -746,24 +753,26 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   return rc;
 }
 
-#ifdef FIBER_TRACE
-// Test build only: record the iterations of pair `pair` into trace (device float4[3*256]);
-// returns nothing; the next fiber_intersect call fills it.  g_trace_n counts records.
-extern "C" int fiber_debug_trace(uint32_t pair, void* trace) {
-  g_trace_pair = pair;
-  g_trace_buf = (float4*)trace;
-  unsigned zero = 0;
-  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
-  return FIBER_OK;
+extern "C" int fiber_traverse(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
+                              const fiber_pair* pairs, int64_t n_pairs, int max_depth,
+                              fiber_hit* hits, void* cuda_stream) {
+  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nullptr,
+                          cuda_stream, STAGE_TRAVERSE);
 }
-#endif
+
+extern "C" int fiber_finalize(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
+                              const fiber_pair* pairs, int64_t n_pairs, int max_depth,
+                              fiber_hit* hits, uint64_t* nearest, void* cuda_stream) {
+  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest,
+                          cuda_stream, STAGE_FINALIZE);
+}
 
 extern "C" int fiber_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                                const fiber_pair* pairs, int64_t n_pairs, int max_depth,
                                fiber_hit* hits, void* cuda_stream) {
   if (n_pairs > 0 && !hits) return set_error(FIBER_EINVAL, "fiber_intersect: NULL hits");
   return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nullptr,
-                          cuda_stream);
+                          cuda_stream, STAGE_TRAVERSE | STAGE_FINALIZE);
 }
 
 extern "C" int fiber_intersect_nearest(const fiber_ray* rays, int64_t n_rays,
@@ -772,7 +781,7 @@ extern "C" int fiber_intersect_nearest(const fiber_ray* rays, int64_t n_rays,
                                        uint64_t* nearest, void* cuda_stream) {
   if (n_pairs > 0 && !nearest) return set_error(FIBER_EINVAL, "fiber_intersect_nearest: NULL nearest");
   return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest,
-                          cuda_stream);
+                          cuda_stream, STAGE_TRAVERSE | STAGE_FINALIZE);
 }
 
 extern "C" int fiber_nearest_init(uint64_t* nearest, int64_t n_rays, void* cuda_stream) {

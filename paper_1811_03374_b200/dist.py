@@ -52,12 +52,30 @@ def nearest_records(nearest_keys: torch.Tensor, hits: torch.Tensor, pairs: torch
 
 
 def gather_records(local: torch.Tensor) -> torch.Tensor:
-    """all_gather of equally sized per-rank record blocks -> [world * n_local, ...]."""
+    """all_gather of equally sized per-rank record blocks -> [world * n_local, ...]
+    (one NCCL all_gather_into_tensor on GPUs; list all_gather on gloo)."""
     world = dist.get_world_size()
-    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
-                      device=local.device)
-    dist.all_gather_into_tensor(out, local.contiguous())
-    return out
+    local = local.contiguous()
+    if dist.get_backend() == "nccl":
+        out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
+        dist.all_gather_into_tensor(out, local)
+        return out
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local)
+    return torch.cat(parts)
+
+
+def nearest_keys_host(t: np.ndarray, hit: np.ndarray, pairs: np.ndarray, n_rays: int) -> np.ndarray:
+    """Host mirror of the K3 epilogue: per ray min((bits(t) << 32) | pair index), -1 = none.
+    (Used to check sharding logic on CPU; the GPU computes it with atomicMin.)"""
+    keys = np.full(n_rays, -1, dtype=np.int64)
+    idx = np.flatnonzero(hit)
+    k = (np.asarray(t, dtype=np.float32)[idx].view(np.uint32).astype(np.uint64) << np.uint64(32)) | \
+        idx.astype(np.uint64)
+    ku = keys.view(np.uint64)
+    np.minimum.at(ku, pairs[idx, 0].astype(np.int64), k)
+    return keys
 
 
 def timed_gather(local: torch.Tensor, iters: int = 3) -> float:
