@@ -111,8 +111,12 @@ __device__ __forceinline__ void get_interval(uint32_t start, uint32_t size, floa
   u1 = __uint_as_float(ui1) - 1.0f;
 }
 
-// Bound tags (which constraint set t_min), F6.
-enum : uint32_t { TAG_ORIGIN = 0, TAG_START = 1, TAG_END = 2, TAG_INTERNAL = 3 };
+// Which constraint bounds t_min (F6, R7).  Every cropping plane -- the slab
+// planes of lst:calc_t_interval and the partition planes of P:1441-1442 -- is the normal
+// plane of the curve at a dyadic parameter u (through C(u), normal parallel to C'(u)), so
+// the tag is that u in 2^-23 units (0 = the start cap, 2^23 = the end cap); TAG_ORIGIN
+// marks the ray origin bound t >= 0.  K3 re-solves crop-plane entries in FP64 from it.
+constexpr uint32_t TAG_ORIGIN = 0xffffffffu;
 
 // The node's own slab: [lo0, hi0] cut by the start plane (through p, normal t0, keeps
 // <x - p, t0> >= 0) and the end plane (through p + d, normal t1, keeps <x - p - d, t1> <= 0)
@@ -122,8 +126,8 @@ enum : uint32_t { TAG_ORIGIN = 0, TAG_START = 1, TAG_END = 2, TAG_INTERNAL = 3 }
 // RE-COMPUTED (lst:recalculation), whose planes can sit a few ulps off the ones the
 // sibling's interval was cut with; without it a hit on the shared plane could fall into
 // the gap between the two intervals.
-__device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, bool u0_is_0,
-                                     bool u1_is_1, float& tmin, float& tmax, uint32_t& tag,
+__device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, uint32_t u0tag,
+                                     uint32_t u1tag, float& tmin, float& tmax, uint32_t& tag,
                                      bool widen = false) {
   tmin = lo0;
   tmax = hi0;
@@ -141,7 +145,7 @@ __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, bool 
   }
   if (z0 > 0.0f) {
     float x = fdiv(n0, z0);
-    if (x > tmin) tmin = x, tag = u0_is_0 ? TAG_START : TAG_INTERNAL;
+    if (x > tmin) tmin = x, tag = u0tag;
   } else if (z0 < 0.0f) {
     tmax = fminf(tmax, fdiv(n0, z0));
   } else if (n0 > 0.0f) {
@@ -149,7 +153,7 @@ __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, bool 
   }
   if (z1 < 0.0f) {
     float x = fdiv(n1, z1);
-    if (x > tmin) tmin = x, tag = u1_is_1 ? TAG_END : TAG_INTERNAL;
+    if (x > tmin) tmin = x, tag = u1tag;
   } else if (z1 > 0.0f) {
     tmax = fminf(tmax, fdiv(n1, z1));
   } else if (n1 < 0.0f) {
@@ -210,7 +214,7 @@ __device__ __forceinline__ void split_geometry(const Delta& c, Split& sp) {
 }
 
 __device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, float& tmin,
-                                           float& tmax, uint32_t& tag, bool crop) {
+                                           float& tmax, uint32_t& tag, bool crop, uint32_t umid) {
   Split sp;
   split_geometry(c, sp);
   float num = dot3(sp.tcn, sp.S), nz = sp.tcn.z;
@@ -223,7 +227,7 @@ __device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, f
   tmax = (apply && up) ? fminf(tmax, tP) : tmax;
   bool lo_up = apply && !up && (tP > tmin);
   tmin = lo_up ? tP : tmin;
-  tag = lo_up ? (uint32_t)TAG_INTERNAL : tag;
+  tag = lo_up ? umid : tag;
   return sp;
 }
 

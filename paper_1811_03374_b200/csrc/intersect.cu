@@ -101,13 +101,13 @@ __device__ __forceinline__ uint32_t encode_oct32(double nx, double ny, double nz
 
 // Re-solves the accepted leaf in FP64.  Lateral entries walk to the neighbouring leaf whose
 // own slab holds the entry point (the FP32 leaf can be a few leaves off at D >= 16, where
-// leaves are narrower than FP32 resolution); cap entries use the global cap plane; crop
-// (WEDGE) and inside entries keep the FP32 parameter t32.
+// leaves are narrower than FP32 resolution); cap and crop-plane (WEDGE) entries re-solve
+// the plane that bounds t_min; inside entries keep t = 0.
 __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, const float4 P0,
                                          const float4 P1, const float4 P2, const float4 P3,
-                                         uint32_t start, int depth, uint32_t kind, float t32,
-                                         float& t_out, float& u_out, uint32_t& n_out,
-                                         bool& hit) {
+                                         uint32_t start, int depth, uint32_t kind,
+                                         uint32_t lo_tag, float t32, float& t_out, float& u_out,
+                                         uint32_t& n_out, bool& hit) {
   const D4 c = D4{0.5 * ((double)P0.x + (double)P3.x), 0.5 * ((double)P0.y + (double)P3.y),
                   0.5 * ((double)P0.z + (double)P3.z), 0.0};
   const D4 q0 = dsub(d4of(P0), c);
@@ -130,6 +130,14 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
     n = c0k ? dscale(-1.0, D0) : D2;
   } else {
     LeafD q = leaf_d(q0, D0, D1, D2, k * inv, (k + 1) * inv);
+    if (kind == FIBER_KIND_WEDGE && lo_tag != TAG_ORIGIN) {
+      // entry through the crop plane that bounds t_min: the normal plane at u = lo_tag
+      // (through C(u), normal C'(u)/3 = H(u, u)), solved in FP64
+      double ul = (double)lo_tag * (1.0 / (double)(1u << FIBER_MAX_DEPTH));
+      LeafD pl = leaf_d(q0, D0, D1, D2, ul, ul + inv);  // p = C(ul), t0 = h H(ul, ul)
+      double wn = ddot3(w, pl.t0);
+      if (wn != 0.0) t = ddot3(dsub(pl.p, m), pl.t0) / wn;
+    }
     if (kind == FIBER_KIND_LATERAL) {
       double te;
       if (leaf_entry(q, m, w, te)) {
@@ -344,7 +352,7 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   cur.d = e.h.D0 + e.h.D1 + e.h.D2;
   cur.t0 = e.h.D0;
   cur.t1 = e.h.D2;
-  slab(cur, e.lo0, e.hi0, true, true, e.tmin, e.tmax, e.tag);
+  slab(cur, e.lo0, e.hi0, 0u, 1u << FIBER_MAX_DEPTH, e.tmin, e.tmax, e.tag);
   return true;
 }
 
@@ -373,7 +381,8 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
     L.c0 = c0;
     return ST_HIT;
   }
-  Split sp = partition(L.cur, c0, c1, L.tmin, L.tmax, L.tag, L.size > kCropMinSize);
+  Split sp = partition(L.cur, c0, c1, L.tmin, L.tmax, L.tag, L.size > kCropMinSize,
+                       L.start + (L.size >> 1));
   // go_down (lst:bitstring_manipulation P:1516-1528)
   L.size >>= 1;
   if (sp.both) {
@@ -420,8 +429,7 @@ __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
     recompute(hs.load(), u0, u1, L.cur);  // lst:recalculation P:1371-1385
   }
   if (L.size >= kCropMinSize) {
-    slab(L.cur, L.lo0, L.hi0, L.start == 0u, L.start + L.size == (1u << FIBER_MAX_DEPTH), L.tmin,
-         L.tmax, L.tag, !cached);
+    slab(L.cur, L.lo0, L.hi0, L.start, L.start + L.size, L.tmin, L.tmax, L.tag, !cached);
     if (L.size == kCropMinSize) {
       L.stmin = L.tmin;
       L.stmax = L.tmax;
@@ -439,7 +447,8 @@ __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
 }
 
 // Pair ended with status st: write the miss, or the provisional hit record for K3
-// (z* bits, start | kind << 24 | inside << 26, 0, counters | bad_segment | kProvisional).
+// (z* bits, start | kind << 24 | inside << 26, tag of t_min, counters | bad_segment |
+// kProvisional).
 __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane& L, int st,
                                          uint32_t badseg) {
   if (st == ST_HIT) {
@@ -448,12 +457,14 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
     uint32_t kind = FIBER_KIND_LATERAL, inside = 0;
     if (!(L.c0 >= L.tmin)) {
       if (L.tag == TAG_ORIGIN) inside = 1, kind = FIBER_KIND_WEDGE;
-      else if (L.tag == TAG_START && L.start == 0u) kind = FIBER_KIND_CAP0;
-      else if (L.tag == TAG_END && L.start + L.size == (1u << FIBER_MAX_DEPTH)) kind = FIBER_KIND_CAP1;
+      else if (L.tag == 0u && L.start == 0u) kind = FIBER_KIND_CAP0;
+      else if (L.tag == (1u << FIBER_MAX_DEPTH) && L.start + L.size == (1u << FIBER_MAX_DEPTH))
+        kind = FIBER_KIND_CAP1;
       else kind = FIBER_KIND_WEDGE;
     }
     if (zs < L.hi0) {  // strictly before the RAY's t_max
-      p.hits[i] = make_float4(zs, __uint_as_float(L.start | (kind << 24) | (inside << 26)), 0.0f,
+      p.hits[i] = make_float4(zs, __uint_as_float(L.start | (kind << 24) | (inside << 26)),
+                              __uint_as_float(L.tag),
                               __uint_as_float(counter_bits(L) | badseg | kProvisional));
       return;
     }
@@ -472,6 +483,7 @@ __device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
   const uint32_t y = __float_as_uint(rec.y);
   uint32_t start = y & 0x00ffffffu, kind = (y >> 24) & 3u;
   bool inside = (y >> 26) & 1u;
+  const uint32_t lo_tag = __float_as_uint(rec.z);
   uint32_t flags = __float_as_uint(rec.w) & ~kProvisional;
   // the FP32 z* as a ray parameter (only used for WEDGE / INSIDE entries)
   Setup32 S;
@@ -481,7 +493,7 @@ __device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
   float t, u;
   uint32_t n_oct;
   bool hit;
-  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, t32, t, u, n_oct, hit);
+  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, lo_tag, t32, t, u, n_oct, hit);
   if (inside && hit) {
     t = 0.0f;
     kind = FIBER_KIND_LATERAL;

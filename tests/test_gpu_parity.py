@@ -1,5 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) vs the FP64 oracle on the same seeded
 inputs, element by element.  Needs a B200."""
+import functools
+
 import numpy as np
 import pytest
 
@@ -19,6 +21,16 @@ def fx():
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     return fx
+
+
+@functools.lru_cache(maxsize=None)
+def _c3(depth):
+    return gen.config3(n_rays=1 << 13, depth=depth)
+
+
+@functools.lru_cache(maxsize=None)
+def _c4(depth):
+    return gen.config4(n_rays=1 << 15, depth=depth)
 
 
 def _run(fx, w, depth=None):
@@ -63,3 +75,36 @@ def test_spec_example_all_depths(fx):
         assert g["hit"][0]
         assert abs(g["t"][0] - 4.9) < 1e-5 and abs(g["u"][0] - 0.5) < 1e-6
         assert np.allclose(g["n"][0], [0, 0, -1], atol=1e-4)
+
+
+@pytest.mark.parametrize("depth", [9, 16])
+def test_config3_hair_parity(fx, depth):
+    """C3 recipe (hair patch, varying radii, 16 candidates per targeted ray), subsampled."""
+    w = _c3(depth)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+    assert rep["hits"] > 500
+
+
+@pytest.mark.parametrize("depth", [4, 12, 22])
+def test_config4_thin_grazing_parity(fx, depth):
+    """C4 recipe (r = 1e-4 chord, half the rays within +-2e-3 r of the silhouette)."""
+    w = _c4(depth)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep, max_excluded_frac=0.7)
+    assert rep["hits"] > 0.5 * (1 << 14)
+
+
+@pytest.mark.parametrize("fiber", ["A", "C"])
+def test_full_size_config2_sampled(fx, fiber):
+    """BASELINE size (2^20 rays, the bench launch) at D = 22: a seeded 8192-pair sample of the
+    full launch compared with the oracle pair by pair."""
+    w = gen.config2(fiber, n_rays=1 << 20, depth=22)
+    g = _run(fx, w)
+    sub = np.sort(np.random.default_rng(9).choice(w.n_pairs, 8192, replace=False))
+    o = oracle.intersect(w.rays, w.ctrl, w.radii, w.pairs[sub], 22)
+    gs = {k: (v[sub] if isinstance(v, np.ndarray) else v) for k, v in g.items()}
+    assert_parity(compare(gs, o))
+    # property at any size: hit fraction as the oracle's sample, counters non-zero
+    assert abs(g["hit"].mean() - o["hit"].mean()) < 0.02
+    assert (g["tests"] >= 1).all()
