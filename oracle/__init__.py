@@ -30,9 +30,10 @@ _lib = None
 OREC = 26
 KIND_LATERAL, KIND_CAP0, KIND_CAP1, KIND_WEDGE, KIND_INSIDE = 0, 1, 2, 3, 4
 
-# grazing band parameters: eps = max(EPS_REL_R * r_max, EPS_ULPS * 2^-24 * S_pair)
+# grazing band (R5): eps = max(EPS_REL_R * r_max, EPS_ULPS * 2^-52 * S_pair) --
+# the north star's 1e-6 r band with an FP64-rounding floor
 EPS_REL_R = 1e-6
-EPS_ULPS = 8.0
+EPS_ULPS = 64.0
 
 
 def build(force: bool = False) -> str:

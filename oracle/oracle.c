@@ -149,34 +149,38 @@ double oracle_conservative_radius(const double Q[16]) {
 }
 
 /* Parameter interval {t : dist(o + t w, line(q, a)) <= R} of an infinite
- * cylinder (the definition Appendix A P:785-874 specialises to unit rays).
- * Returns 0 if empty, 1 if [*c0, *c1] (c0 = -inf, c1 = +inf when the ray is
- * parallel to the axis and inside, F4). */
+ * cylinder.  Written in the closest-approach form of Appendix A: with
+ * n = w x a^, the squared line-line distance d^2 = <o - q, n>^2 / |n|^2 (eq. P:814), the
+ * parameter of closest approach t_cpa and the half chord
+ * s = sqrt((R^2 - d^2) / |n|^2), since |(o + t w - q) x a^|^2 =
+ * d^2 + |n|^2 (t - t_cpa)^2.  (This form keeps full precision for rays that pass close to
+ * tangency, where expanding the quadratic cancels.)  Returns 0 if empty, 1 if [*c0, *c1]
+ * (c0 = -inf, c1 = +inf when the ray is parallel to the axis and inside, F4). */
 int oracle_cylinder(const double o[3], const double w[3], const double q[3], const double a[3],
                     double R, double *c0, double *c1) {
   double la = norm3(a);
   double ah[3] = {a[0] / la, a[1] / la, a[2] / la};
-  double m[3], mx[3], wx[3];
+  double m[3], n[3], mx[3];
   sub3(o, q, m);
-  cross3(m, ah, mx); /* (o - q) x a^ */
-  cross3(w, ah, wx); /* w x a^       */
-  /* |mx + t wx|^2 = R^2  <=>  A t^2 + 2 B t + C = 0 */
-  double A = dot3(wx, wx);
-  double B = dot3(mx, wx);
-  double C = dot3(mx, mx) - R * R;
+  cross3(w, ah, n); /* w x a^ */
+  double A = dot3(n, n);
   if (A == 0.0) { /* F4: ray parallel to the axis */
-    if (C <= 0.0) {
+    cross3(m, ah, mx);
+    if (dot3(mx, mx) <= R * R) {
       *c0 = -INFINITY;
       *c1 = INFINITY;
       return 1;
     }
     return 0;
   }
-  double disc = B * B - A * C;
-  if (disc < 0.0) return 0;
-  double s = sqrt(disc);
-  *c0 = (-B - s) / A;
-  *c1 = (-B + s) / A;
+  double mn = dot3(m, n);
+  double d2 = mn * mn / A; /* squared distance between the ray line and the axis */
+  if (d2 > R * R) return 0;
+  cross3(m, ah, mx);
+  double tcpa = -dot3(mx, n) / A;
+  double s = sqrt((R * R - d2) / A);
+  *c0 = tcpa - s;
+  *c1 = tcpa + s;
   return 1;
 }
 
@@ -401,8 +405,9 @@ static opair run_pair(octx *c) {
 }
 
 /* ------------------------------------------------------------------ */
-/* grazing band width                              */
-/* eps = max(1e-6 * r_max, 8 * 2^-24 * S_pair), S_pair = largest |coordinate|
+/* grazing band width (R5)                          */
+/* eps = max(eps_rel_r * r_max, eps_ulps * 2^-52 * S_pair): the north star's 1e-6 r band,
+ * with an FP64-rounding floor; S_pair = largest |coordinate|
  * of the control points relative to o' = o + <c - o, w^> w^, c = (P0+P3)/2 */
 /* ------------------------------------------------------------------ */
 static double pair_eps(const octx *c, double eps_rel_r, double eps_ulps) {
@@ -418,7 +423,7 @@ static double pair_eps(const octx *c, double eps_rel_r, double eps_ulps) {
     for (int k = 0; k < 3; ++k) S = fmax(S, fabs(c->P[4 * i + k] - op[k]));
     rmax = fmax(rmax, c->P[4 * i + 3]);
   }
-  return fmax(eps_rel_r * rmax, eps_ulps * ldexp(1.0, -24) * S);
+  return fmax(eps_rel_r * rmax, eps_ulps * ldexp(1.0, -52) * S);
 }
 
 /* ------------------------------------------------------------------ */

@@ -128,7 +128,7 @@ constexpr uint32_t TAG_ORIGIN = 0xffffffffu;
 // the gap between the two intervals.
 __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, uint32_t u0tag,
                                      uint32_t u1tag, float& tmin, float& tmax, uint32_t& tag,
-                                     bool widen = false) {
+                                     bool widen = false, float* kappa = nullptr) {
   tmin = lo0;
   tmax = hi0;
   tag = TAG_ORIGIN;
@@ -159,6 +159,11 @@ __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, uint3
   } else if (n1 < 0.0f) {
     tmin = INFINITY;
   }
+  if (kappa) {  // conditioning of the two crossings: |t|_1 / |t_z| (>= 1 / cos)
+    float k0 = (fabsf(c.t0.x) + fabsf(c.t0.y) + fabsf(z0)) * frcp(fabsf(z0));
+    float k1 = (fabsf(c.t1.x) + fabsf(c.t1.y) + fabsf(z1)) * frcp(fabsf(z1));
+    *kappa = fminf(fmaxf(k0, k1), 1e30f);
+  }
 }
 
 // Descent-time crop limit: partition planes crop the ray interval
@@ -174,7 +179,8 @@ constexpr uint32_t kCropMinSize = 1u << (FIBER_MAX_DEPTH - kCropLevel);
 // x infinite cylinder of App. A (lst:ray-cylinder P:1279-1303, eq. P:814, t_cpa P:825-833,
 // s P:862-866).  F4: an axis parallel to the ray gives the whole line if inside.  F5: a
 // miss is reported as `false`, never as a sentinel interval.
-__device__ __forceinline__ bool cylinder(const Delta& c, float& c0, float& c1) {
+__device__ __forceinline__ bool cylinder(const Delta& c, float& c0, float& c1, float* tie_e = nullptr,
+                                         float* inv_sin = nullptr, float delta = 0.0f) {
   float dd = dot3(c.d, c.d);
   float m2 = fmaxf(cross_norm2(c.t0, c.d), cross_norm2(c.t1, c.d));
   float dist = fsqrt(m2 * frcp(dd));
@@ -191,6 +197,13 @@ __device__ __forceinline__ bool cylinder(const Delta& c, float& c0, float& c1) {
   bool in = fmaf(c.p.x, c.p.x, c.p.y * c.p.y) <= R * R;
   c0 = par ? -INFINITY : tc - s;
   c1 = par ? INFINITY : tc + s;
+  if (tie_e) {
+    // near-tie of the distance test |R - dist| against the error of FP32 coordinates
+    // (delta) and a relative 2^-12 (R5): flags the pair for the FP64 re-run
+    float ee = par ? fmaf(R, R, -fmaf(c.p.x, c.p.x, c.p.y * c.p.y)) : e;
+    *tie_e = fabsf(ee) - R * fmaf(2.44140625e-4f, R, 4.0f * delta);  // < 0: tie
+    *inv_sin = fsqrt(dd * h);                                        // 1 / sin(ray, axis)
+  }
   return par ? in : (e >= 0.0f);
 }
 
@@ -203,7 +216,6 @@ __device__ __forceinline__ bool cylinder(const Delta& c, float& c0, float& c1) {
 //   left = (p, dp, t0/2, t_c),   right = (p + dp, d - dp, t_c, t1/2).
 struct Split {
   float4 dp, tcn, S;
-  bool right, both;
 };
 
 // Split point and tangent of node c (3.1): delta_p, t_c and S = p + delta_p.
@@ -214,14 +226,17 @@ __device__ __forceinline__ void split_geometry(const Delta& c, Split& sp) {
 }
 
 __device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, float& tmin,
-                                           float& tmax, uint32_t& tag, bool crop, uint32_t umid) {
+                                           float& tmax, uint32_t& tag, bool crop, uint32_t umid,
+                                           bool& right, bool& both, float& tP, float& kappa) {
   Split sp;
   split_geometry(c, sp);
   float num = dot3(sp.tcn, sp.S), nz = sp.tcn.z;
-  float tP = num * frcp(nz);
+  float rz = frcp(nz);
+  tP = num * rz;
+  kappa = fminf((fabsf(sp.tcn.x) + fabsf(sp.tcn.y) + fabsf(nz)) * fabsf(rz), 1e30f);
   bool par = (nz == 0.0f);
-  sp.right = par ? (num < 0.0f) : ((tP > c0) != (nz > 0.0f));
-  sp.both = !par && (c0 < tP) && (tP < c1);
+  right = par ? (num < 0.0f) : ((tP > c0) != (nz > 0.0f));
+  both = !par && (c0 < tP) && (tP < c1);
   bool up = tP > c0;
   bool apply = crop && !par;
   tmax = (apply && up) ? fminf(tmax, tP) : tmax;

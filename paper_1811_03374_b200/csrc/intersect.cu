@@ -12,6 +12,7 @@
 #include <mutex>
 
 #include "fiber.h"
+#include "exact.cuh"
 #include "fiber_device.cuh"
 #include "fiber_internal.h"
 
@@ -63,7 +64,9 @@ __device__ __forceinline__ LeafD leaf_d(D4 q0, D4 D0, D4 D1, D4 D2, double u0, d
 }
 
 // Entry parameter t of the ray m + t w (m relative to the anchor) into the infinite
-// conservative cylinder of leaf q (App. A's definition), FP64, stable roots.
+// conservative cylinder of leaf q, FP64, in App. A's closest-approach form
+// (d^2 of eq. P:814, t_cpa P:825-833, s P:862-866) with n = w x d, which keeps full
+// precision near tangency (the expanded quadratic would cancel).
 __device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t) {
   double dd = ddot3(q.d, q.d);
   D4 x0 = dcross(q.t0, q.d), x1 = dcross(q.t1, q.d);
@@ -71,13 +74,15 @@ __device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t
   double maxr = q.p.w + fmax(fmax(0.0, q.t0.w), fmax(q.d.w, q.d.w - q.t1.w));
   double R = sqrt(m2 / dd) + maxr;
   D4 mm = dsub(m, q.p);
-  D4 md = dcross(mm, q.d), wd = dcross(w, q.d);
-  double A = ddot3(wd, wd), B = ddot3(md, wd), C = fma(-R * R, dd, ddot3(md, md));
-  double disc = fma(B, B, -A * C);
-  if (!(A > 0.0) || !(disc >= 0.0)) return false;
-  double qq = -(B + copysign(sqrt(disc), B));
-  double r0 = qq / A, r1 = C / qq;
-  t = fmin(r0, r1);
+  D4 n = dcross(w, q.d);            // |n|^2 = |w x d|^2
+  double A = ddot3(n, n);
+  if (!(A > 0.0)) return false;
+  double mn = ddot3(mm, n);
+  double d2 = mn * mn / A;          // squared line-line distance (eq. P:814)
+  if (!(d2 <= R * R)) return false;
+  D4 md = dcross(mm, q.d);
+  double tcpa = -ddot3(md, n) / A;
+  t = tcpa - sqrt((R * R - d2) * dd / A);
   return isfinite(t);
 }
 
@@ -106,8 +111,8 @@ __device__ __forceinline__ uint32_t encode_oct32(double nx, double ny, double nz
 __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, const float4 P0,
                                          const float4 P1, const float4 P2, const float4 P3,
                                          uint32_t start, int depth, uint32_t kind,
-                                         uint32_t lo_tag, float t32, float& t_out, float& u_out,
-                                         uint32_t& n_out, bool& hit) {
+                                         uint32_t lo_tag, float t32, int walk, float& t_out,
+                                         float& u_out, uint32_t& n_out, bool& hit) {
   const D4 c = D4{0.5 * ((double)P0.x + (double)P3.x), 0.5 * ((double)P0.y + (double)P3.y),
                   0.5 * ((double)P0.z + (double)P3.z), 0.0};
   const D4 q0 = dsub(d4of(P0), c);
@@ -143,7 +148,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
       if (leaf_entry(q, m, w, te)) {
         t = te;
         int dir = 0;
-        for (int it = 0; it < 64; ++it) {
+        for (int it = 0; it < walk; ++it) {
           // side of the entry point w.r.t. the leaf's own start / end planes
           D4 X = dsub(D4{fma(t, w.x, m.x), fma(t, w.y, m.y), fma(t, w.z, m.z), 0.0}, q.p);
           double side0 = ddot3(X, q.t0);
@@ -230,8 +235,9 @@ struct Params {
   uint32_t min_size;  // 2^(23 - depth), lst:algorithm
   float4* hits;
   unsigned long long* nearest;
-  unsigned int* counter;  // slot: [0] K2 pair counter, [1] K3 chunk counter,
-                          // [2] K2 blocks done, [3] K3 blocks done (all zero at launch)
+  unsigned int* counter;  // slot: [0] K2 pair counter, [1] K3 chunk counter, [2] K2 blocks
+                          // done, [3] K3 blocks done, [4] K4 chunk counter, [5] K4 blocks
+                          // done (all zero at launch)
 #ifdef FIBER_TRACE
   uint32_t trace_pair;  // test build only: per-iteration records of one pair
   float4* trace;        // [kTraceCap] x 3 float4
@@ -242,8 +248,12 @@ constexpr int kTraceCap = 256;
 __device__ unsigned int g_trace_n;
 #endif
 
-// Internal flag of a provisional record (never visible after fiber_intersect returns).
+// Internal flags of records between the kernels (never visible after fiber_intersect
+// returns): a provisional hit for K3, an undecided pair for K4.
 constexpr uint32_t kProvisional = 1u << 6;
+constexpr uint32_t kUncertain = 1u << 7;
+constexpr uint32_t kExactLeaf = 1u << 27;  // in word y of a provisional record: K4's leaf
+constexpr int kWalk = 48;                  // K3's neighbour-leaf walk range
 
 __device__ __forceinline__ void write_record(const Params& p, uint32_t i, uint32_t ray, float t,
                                              float u, uint32_t n_oct, uint32_t flags) {
@@ -267,6 +277,9 @@ struct Lane {
   Delta cur;
   float tmin, tmax, lo0, hi0, c0;
   float stmin, stmax;  // interval saved at level kCropLevel (deep backtracks)
+  float delta;         // FP32 error scale of the local coordinates: 2^-20 max|coordinate|
+  float terr, sterr;   // error bound of the current (saved) interval bounds
+  bool tie;            // a decision was a near-tie: re-run the pair in FP64 (K4)
   uint32_t tag, stag, bits, start, size, tests, backtracks;
   uint32_t ncache, cache_top, cache_right;  // parent-cache fill, ring top, near-side bits
 };
@@ -312,7 +325,7 @@ struct HodoRef {
 // One prepared pair: the ray-frame curve, the ray interval and the root slab.
 struct Prepared {
   Hodo h;
-  float lo0, hi0, tmin, tmax;
+  float lo0, hi0, tmin, tmax, delta, terr;
   uint32_t pair, badseg, tag;
 };
 
@@ -352,7 +365,13 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   cur.d = e.h.D0 + e.h.D1 + e.h.D2;
   cur.t0 = e.h.D0;
   cur.t1 = e.h.D2;
-  slab(cur, e.lo0, e.hi0, 0u, 1u << FIBER_MAX_DEPTH, e.tmin, e.tmax, e.tag);
+  float kappa;
+  slab(cur, e.lo0, e.hi0, 0u, 1u << FIBER_MAX_DEPTH, e.tmin, e.tmax, e.tag, false, &kappa);
+  // FP32 error scale: 2^-20 of the largest local coordinate of the control points
+  const float4 L1 = e.h.L0 + e.h.D0, L3 = e.h.L0 + cur.d, L2 = L3 - e.h.D2;
+  auto amax = [](float4 v) { return fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z))); };
+  e.delta = 9.5367431640625e-07f * fmaxf(fmaxf(amax(e.h.L0), amax(L1)), fmaxf(amax(L2), amax(L3)));
+  e.terr = e.delta * fmaf(4.0f, kappa, 4.0f);
   return true;
 }
 
@@ -361,10 +380,17 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
 __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
                                     float4* trace = nullptr) {
   ++L.tests;
-  float c0, c1;
-  bool pass = cylinder(L.cur, c0, c1);
+  float c0, c1, tie_e, inv_sin;
+  const bool cyl = cylinder(L.cur, c0, c1, &tie_e, &inv_sin, L.delta);
   // pruning test P:1618 with F1 (empty interval) and F5 (explicit miss)
-  pass = pass && (c1 >= L.tmin) && (c0 <= L.tmax) && (L.tmin <= L.tmax);
+  bool pass = cyl && (c1 >= L.tmin) && (c0 <= L.tmax) && (L.tmin <= L.tmax);
+  // near-ties of the test (R5): the entry/exit parameters carry an error of about
+  // delta / sin(ray, axis), the interval bounds L.terr
+  const float tau = L.delta * fmaf(8.0f, inv_sin, 8.0f);
+  const float tb = tau + L.terr;
+  L.tie |= (tie_e < 0.0f) ||
+           (cyl && ((fabsf(c1 - L.tmin) < tb) | (fabsf(L.tmax - c0) < tb) |
+                    (fabsf(L.tmax - L.tmin) < 2.0f * L.terr)));
 #ifdef FIBER_TRACE
   if (trace) {
     unsigned k = atomicAdd(&g_trace_n, 1u);
@@ -378,29 +404,47 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
 #endif
   if (!pass) return L.bits == 0u ? ST_MISS : ST_NEED_BT;  // done / backtrack
   if (L.size <= min_size) {  // leaf: first hit terminates
+    L.tie |= fabsf(c0 - L.tmin) < tb;  // the kind decision (F2, F6)
+    // below the crop level the leaf index is only known to about (error of c0 along the
+    // axis) / (leaf length) = tau |d_z| / |d|^2 leaves; K3 walks up to kWalk of them, so
+    // nearly parallel rays that could be further off are re-run in FP64
+    if (L.size < kCropMinSize)
+      L.tie |= tau * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d);
     L.c0 = c0;
     return ST_HIT;
   }
+  bool right, both;
+  float tP, kP;
+  const float tmin_in = L.tmin, tmax_in = L.tmax;
   Split sp = partition(L.cur, c0, c1, L.tmin, L.tmax, L.tag, L.size > kCropMinSize,
-                       L.start + (L.size >> 1));
+                       L.start + (L.size >> 1), right, both, tP, kP);
+  if (L.size > kCropMinSize) {
+    // near-ties of the near-child / both decisions and the error of the updated bound.
+    // Below the crop level these decisions only pick among nearly collinear leaves (the
+    // FP64 finalisation walks to the right one), so they are not re-run.
+    const float tauP = L.delta * fmaf(4.0f, kP, 4.0f);
+    L.tie |= (fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP);
+    if (L.tmin != tmin_in || L.tmax != tmax_in) L.terr = fmaxf(L.terr, tauP);
+  }
   // go_down (lst:bitstring_manipulation P:1516-1528)
   L.size >>= 1;
-  if (sp.both) {
+  if (both) {
     // remember the parent: the next jump_up returns to the deepest pending level, i.e.
     // the most recent push (LIFO); the ring drops the oldest entry when full
     L.bits |= L.size;
     L.cache_top = (L.cache_top + 1u) % kFarCache;
     hs.push(L.cur, L.cache_top);
-    L.cache_right = sp.right ? (L.cache_right | (1u << L.cache_top))
+    L.cache_right = right ? (L.cache_right | (1u << L.cache_top))
                              : (L.cache_right & ~(1u << L.cache_top));
     L.ncache = min(L.ncache + 1u, (uint32_t)kFarCache);
   }
-  if (sp.right) L.start |= L.size;
-  child(L.cur, sp, sp.right, L.cur);
+  if (right) L.start |= L.size;
+  child(L.cur, sp, right, L.cur);
   if (L.size == kCropMinSize) {
     L.stmin = L.tmin;
     L.stmax = L.tmax;
     L.stag = L.tag;
+    L.sterr = L.terr;
   }
   return ST_RUNNING;
 }
@@ -429,16 +473,20 @@ __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
     recompute(hs.load(), u0, u1, L.cur);  // lst:recalculation P:1371-1385
   }
   if (L.size >= kCropMinSize) {
-    slab(L.cur, L.lo0, L.hi0, L.start, L.start + L.size, L.tmin, L.tmax, L.tag, !cached);
+    float kappa;
+    slab(L.cur, L.lo0, L.hi0, L.start, L.start + L.size, L.tmin, L.tmax, L.tag, !cached, &kappa);
+    L.terr = L.delta * fmaf(4.0f, kappa, 4.0f) * (cached ? 1.0f : 4.0f);
     if (L.size == kCropMinSize) {
       L.stmin = L.tmin;
       L.stmax = L.tmax;
       L.stag = L.tag;
+      L.sterr = L.terr;
     }
   } else {
     L.tmin = L.stmin;
     L.tmax = L.stmax;
     L.tag = L.stag;
+    L.terr = L.sterr;
   }
 }
 
@@ -451,6 +499,10 @@ __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
 // kProvisional).
 __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane& L, int st,
                                          uint32_t badseg) {
+  if (L.tie) {  // decided by a near-tie somewhere: K4 re-runs the pair in FP64
+    p.hits[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(badseg | kUncertain));
+    return;
+  }
   if (st == ST_HIT) {
     // F2: entry into the cropped cylinder; F6: kind from the binding constraint
     float zs = fmaxf(L.c0, L.tmin);
@@ -483,6 +535,7 @@ __device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
   const uint32_t y = __float_as_uint(rec.y);
   uint32_t start = y & 0x00ffffffu, kind = (y >> 24) & 3u;
   bool inside = (y >> 26) & 1u;
+  const bool exact_leaf = (y & kExactLeaf) != 0u;
   const uint32_t lo_tag = __float_as_uint(rec.z);
   uint32_t flags = __float_as_uint(rec.w) & ~kProvisional;
   // the FP32 z* as a ray parameter (only used for WEDGE / INSIDE entries)
@@ -493,7 +546,8 @@ __device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
   float t, u;
   uint32_t n_oct;
   bool hit;
-  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, lo_tag, t32, t, u, n_oct, hit);
+  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, lo_tag, t32, exact_leaf ? 0 : kWalk,
+           t, u, n_oct, hit);
   if (inside && hit) {
     t = 0.0f;
     kind = FIBER_KIND_LATERAL;
@@ -538,6 +592,9 @@ __device__ __forceinline__ void start_lane(const Prepared& e, Lane& L, HodoRef h
   L.tmin = L.stmin = e.tmin;
   L.tmax = L.stmax = e.tmax;
   L.tag = L.stag = e.tag;
+  L.delta = e.delta;
+  L.terr = L.sterr = e.terr;
+  L.tie = false;
   L.bits = 0;
   L.size = 1u << FIBER_MAX_DEPTH;
   L.start = 0;
@@ -549,7 +606,10 @@ __device__ __forceinline__ void start_lane(const Prepared& e, Lane& L, HodoRef h
   L.cache_right = 0;
 }
 
-__global__ void __launch_bounds__(kThreads, 3) intersect_kernel(const Params p) {
+#ifndef FIBER_K2_MINBLOCKS
+#define FIBER_K2_MINBLOCKS 3
+#endif
+__global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel(const Params p) {
   extern __shared__ float4 smem[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
@@ -603,10 +663,71 @@ __global__ void __launch_bounds__(kThreads, 3) intersect_kernel(const Params p) 
 }
 
 // ------------------------------------------------------------------------------------
+// K4, the FP64 re-run of the pairs K2 flagged as decided by a near-tie (R5):
+// scans the records, queues flagged pairs per warp and traverses them 32 at a time in
+// double precision (exact.cuh), leaving a provisional record for K3 or the final miss.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void exact_one(const Params& p, uint32_t i) {
+  const uint32_t badseg = __float_as_uint(p.hits[i].w) & FIBER_BAD_SEGMENT;
+  const uint2 pr = __ldg(&p.pairs[i]);
+  const float4 ray0 = __ldg(&p.rays[2 * (int64_t)pr.x]);
+  const float4 ray1 = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
+  const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
+  const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
+  const exact::Result r = exact::traverse(ray0, ray1, P0, P1, P2, P3, p.depth);
+  const uint32_t cnt = (min(r.backtracks, 255u) << 8) | (min(r.tests, 65535u) << 16);
+  if (r.hit) {
+    p.hits[i] = make_float4(0.0f, __uint_as_float(r.start | (r.kind << 24) | (r.inside << 26) | kExactLeaf),
+                            __uint_as_float(r.tag), __uint_as_float(cnt | badseg | kProvisional));
+  } else {
+    p.hits[i] = make_float4(INFINITY, 0.0f, 0.0f, __uint_as_float(cnt | badseg));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) exact_kernel(const Params p) {
+  __shared__ uint32_t s_q[kWarps][kQueue];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t nq = 0;
+  auto flush = [&](uint32_t take) {
+    if (lane < take) exact_one(p, s_q[wid][lane]);
+    __syncwarp();
+    uint32_t mv = 0;
+    bool has = lane + take < nq;
+    if (has) mv = s_q[wid][lane + take];
+    __syncwarp();
+    if (has) s_q[wid][lane] = mv;
+    nq -= take;
+    __syncwarp();
+  };
+  while (true) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&p.counter[4], 128u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= p.n_pairs) break;
+    for (uint32_t k = 0; k < 128u; k += 32u) {
+      const uint32_t i = base + k + lane;
+      bool unc = false;
+      if (i < p.n_pairs) unc = (__float_as_uint(p.hits[i].w) & kUncertain) != 0u;
+      unsigned m = __ballot_sync(0xffffffffu, unc);
+      if (unc) s_q[wid][nq + __popc(m & lt)] = i;
+      nq += __popc(m);
+      __syncwarp();
+      if (nq >= 32u) flush(32u);
+    }
+  }
+  while (nq > 0u) flush(min(nq, 32u));
+  release_counter(p.counter, 4, 5);
+}
+
+// ------------------------------------------------------------------------------------
 // K3, the finalisation kernel: scans the records, queues provisional hits per warp and
 // finalises them in FP64 32 at a time (converged).  a7, lst:calc_intersection P:1546-1587.
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 2) finalize_kernel(const Params p) {
+#ifndef FIBER_K3_MINBLOCKS
+#define FIBER_K3_MINBLOCKS 2
+#endif
+__global__ void __launch_bounds__(kThreads, FIBER_K3_MINBLOCKS) finalize_kernel(const Params p) {
   __shared__ uint32_t s_q[kWarps][kQueue];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
@@ -655,10 +776,11 @@ using namespace fiberx;
 // Per-device launch constants, queried once per process and device (immutable afterwards;
 // a call otherwise spends far longer in these queries than the GPU spends on 1M pairs).
 struct LaunchInfo {
-  int sms, k2_per_sm, k3_per_sm;
+  int sms, k2_per_sm, k3_per_sm, k4_per_sm;
   unsigned int* slots;  // kSlots x 4 work counters, zero between uses
 };
 constexpr int kSlots = 1024;  // calls in flight on one device at a time (any streams)
+constexpr int kSlotWords = 8;
 static std::atomic<unsigned> g_next_slot{0};
 
 static const LaunchInfo* launch_info() {
@@ -676,10 +798,12 @@ static const LaunchInfo* launch_info() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k2_per_sm, intersect_kernel, kThreads,
                                                   kSmemBytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k3_per_sm, finalize_kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k4_per_sm, exact_kernel, kThreads, 0);
+    if (li.k4_per_sm < 1) li.k4_per_sm = 1;
     if (li.k2_per_sm < 1) li.k2_per_sm = 1;
     if (li.k3_per_sm < 1) li.k3_per_sm = 1;
-    if (cudaMalloc((void**)&li.slots, kSlots * 4 * sizeof(unsigned int)) != cudaSuccess) return nullptr;
-    if (cudaMemset(li.slots, 0, kSlots * 4 * sizeof(unsigned int)) != cudaSuccess) return nullptr;
+    if (cudaMalloc((void**)&li.slots, kSlots * kSlotWords * sizeof(unsigned int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(li.slots, 0, kSlots * kSlotWords * sizeof(unsigned int)) != cudaSuccess) return nullptr;
     if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
     if (cudaGetLastError() != cudaSuccess || li.sms < 1) return nullptr;
     info[dev] = li;
@@ -714,7 +838,7 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   if (!li) return set_error(FIBER_ECUDA, "fiber_intersect: device query failed");
   // work counters: a self-resetting slot of the per-device pool (no per-call allocation);
   // scratch records only when the caller passes no hits buffer (nearest-only calls)
-  unsigned int* counter = li->slots + 4 * (g_next_slot.fetch_add(1u) % kSlots);
+  unsigned int* counter = li->slots + kSlotWords * (g_next_slot.fetch_add(1u) % kSlots);
   void* scratch = nullptr;
   if (!hits) {
     cudaError_t e = cudaMallocAsync(&scratch, (size_t)n_pairs * sizeof(fiber_hit), st);
@@ -752,6 +876,15 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
     if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
     intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
     rc = check_launch("fiber_intersect (traverse)");
+#ifndef FIBER_NO_EXACT
+    if (rc == FIBER_OK) {  // FP64 re-run of near-tie pairs (part of the traversal stage)
+      int64_t xblocks = (int64_t)li->sms * li->k4_per_sm;
+      int64_t xchunks = (n_pairs + 127) / 128;
+      if (xblocks * kWarps > xchunks) xblocks = (xchunks + kWarps - 1) / kWarps;
+      exact_kernel<<<(unsigned)xblocks, kThreads, 0, st>>>(p);
+      rc = check_launch("fiber_intersect (exact)");
+    }
+#endif
   }
   if (rc == FIBER_OK && (stages & STAGE_FINALIZE)) {
     int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;

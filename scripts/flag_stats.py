@@ -1,0 +1,19 @@
+"""Fraction of pairs K2 flags for the FP64 re-run (noexact build)."""
+import os
+import sys
+
+os.environ["FIBER_LIB_VARIANT"] = "noexact"
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+
+import paper_1811_03374_b200 as fx  # noqa: E402
+from workloads import gen  # noqa: E402
+
+for name, w in (("C2A", gen.config2("A", n_rays=1 << 18, depth=22)),
+                ("C2A9", gen.config2("A", n_rays=1 << 18, depth=9)),
+                ("C2A2", gen.config2("A", n_rays=1 << 18, depth=2)),
+                ("C4", gen.config4(n_rays=1 << 15, depth=22))):
+    rays, segs, pairs = fx.to_device(w)
+    h = fx.intersect(rays, segs, pairs, w.depth)
+    f = h.cpu().numpy().view(np.uint32)[:, 3]
+    print(name, "flagged", ((f >> 7) & 1).mean(), flush=True)

@@ -14,7 +14,10 @@ from workloads import gen  # noqa: E402
 
 fiber, depth, mode, idx = sys.argv[1], int(sys.argv[2]), sys.argv[3], int(sys.argv[4])
 n = int(sys.argv[5]) if len(sys.argv) > 5 else 1 << 15
-w = gen.config2(fiber, n_rays=n, depth=depth, targeted=(mode == "t"))
+if fiber == "C4":
+    w = gen.config4(n_rays=n, depth=depth)
+else:
+    w = gen.config2(fiber, n_rays=n, depth=depth, targeted=(mode == "t"))
 L = fx.lib()
 L.fiber_debug_trace.argtypes = [ctypes.c_uint32, ctypes.c_void_p]
 buf = torch.zeros((256 * 3, 4), dtype=torch.float32, device="cuda")
@@ -32,10 +35,12 @@ for k in range(int(g["tests"][idx])):
     lvl = 23 - int(size).bit_length() + 1
     print(f"  it{k:2d} lvl {lvl:2d} u0 {start / 2**23:.9f} size {size:8d} bits {bits:08x} pass {pas} "
           f"c0 {r1[0]: .9e} c1 {r1[1]: .9e} tmin {r1[2]: .9e} tmax {r1[3]: .9e} tag {r2[0]} nc {r2[1]}")
-res, tr = oracle.trace(w.rays[idx], w.ctrl[0], w.radii[0], depth)
+seg = int(w.pairs[idx, 1])
+ray = w.rays[int(w.pairs[idx, 0])]
+res, tr = oracle.trace(ray, w.ctrl[seg], w.radii[seg], depth)
 print("oracle: hit", res[5], "t", res[0], "u", res[1], "tests", res[7], "bt", res[8], "kind", res[6])
 for l, u0, u1, ev in tr:
     print(f"  lvl {int(l):2d} u0 {u0:.9f} u1 {u1:.9f} ev {int(ev)}")
 for sgn in (+1, -1):
-    res2, _ = oracle.trace(w.rays[idx], w.ctrl[0], w.radii[0], depth, signed_eps=sgn * 2.5e-7)
+    res2, _ = oracle.trace(ray, w.ctrl[seg], w.radii[seg], depth, signed_eps=sgn * 1e-6 * float(w.radii[seg].max()))
     print("oracle eps", sgn, "hit", res2[5], "t", res2[0], "tests", res2[7])

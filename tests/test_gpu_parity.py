@@ -91,7 +91,7 @@ def test_config4_thin_grazing_parity(fx, depth):
     """C4 recipe (r = 1e-4 chord, half the rays within +-2e-3 r of the silhouette)."""
     w = _c4(depth)
     rep = compare(_run(fx, w), _oracle(w))
-    assert_parity(rep, max_excluded_frac=0.7)
+    assert_parity(rep, max_excluded_frac=0.1)
     assert rep["hits"] > 0.5 * (1 << 14)
 
 
