@@ -86,20 +86,21 @@ __device__ __forceinline__ void slab(const Curve& c, double lo0, double hi0, uin
 
 // unit ray x conservative cylinder (App. A), F4 for an axis parallel to the ray
 __device__ __forceinline__ bool cylinder(const Curve& c, double& c0, double& c1) {
-  double dd = dot3(c.d, c.d);
+  double g = fma(c.d.x, c.d.x, c.d.y * c.d.y);
+  double dd = fma(c.d.z, c.d.z, g);
   double m2 = fmax(crossn2(c.t0, c.d), crossn2(c.t1, c.d));
   double R = sqrt(m2 / dd) + c.p.w + fmax(fmax(0.0, c.t0.w), fmax(c.d.w, c.d.w - c.t1.w));
-  double g = fma(c.d.x, c.d.x, c.d.y * c.d.y);
   if (g == 0.0) {
     c0 = -INFINITY;
     c1 = INFINITY;
     return fma(c.p.x, c.p.x, c.p.y * c.p.y) <= R * R;
   }
+  const double ig = 1.0 / g;
   double dxy = fma(c.d.x, c.p.y, -c.d.y * c.p.x);
-  double e = R * R - dxy * dxy / g;
+  double e = fma(-dxy * dxy, ig, R * R);
   if (!(e >= 0.0)) return false;
-  double tc = c.p.z - c.d.z * fma(c.d.x, c.p.x, c.d.y * c.p.y) / g;
-  double s = sqrt(e * dd / g);
+  double tc = fma(-c.d.z * ig, fma(c.d.x, c.p.x, c.d.y * c.p.y), c.p.z);
+  double s = sqrt(e * dd * ig);
   c0 = tc - s;
   c1 = tc + s;
   return true;
@@ -112,7 +113,7 @@ struct Result {
 };
 
 // The whole traversal of one pair in FP64.
-__device__ __noinline__ Result traverse(const float4 ray0, const float4 ray1, const float4 P0,
+__device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1, const float4 P0,
                                         const float4 P1, const float4 P2, const float4 P3,
                                         int depth) {
   Result res{false, 0, 0, 0, 0, kOrigin, 0, 0, 0.0};

@@ -171,7 +171,10 @@ __device__ __forceinline__ void slab(const Delta& c, float lo0, float hi0, uint3
 // segment) falls under FP32 resolution of the plane crossings, so its bounds would invert
 // by rounding; deeper nodes inherit the level-kCropLevel interval, and the planes still
 // order the children.  The FP64 finalisation then re-solves the exact leaf.
-constexpr int kCropLevel = 15;
+#ifndef FIBER_CROP_LEVEL
+#define FIBER_CROP_LEVEL 12
+#endif
+constexpr int kCropLevel = FIBER_CROP_LEVEL;
 constexpr uint32_t kCropMinSize = 1u << (FIBER_MAX_DEPTH - kCropLevel);
 
 // Node test (a3): conservative radius (lst:calc_radius P:1415-1425 with the point-line
@@ -199,9 +202,9 @@ __device__ __forceinline__ bool cylinder(const Delta& c, float& c0, float& c1, f
   c1 = par ? INFINITY : tc + s;
   if (tie_e) {
     // near-tie of the distance test |R - dist| against the error of FP32 coordinates
-    // (delta) and a relative 2^-12 (R5): flags the pair for the FP64 re-run
+    // (delta) and a relative 2^-16 (R5): flags the pair for the FP64 re-run
     float ee = par ? fmaf(R, R, -fmaf(c.p.x, c.p.x, c.p.y * c.p.y)) : e;
-    *tie_e = fabsf(ee) - R * fmaf(2.44140625e-4f, R, 4.0f * delta);  // < 0: tie
+    *tie_e = fabsf(ee) - R * fmaf(1.52587890625e-05f, R, 2.0f * delta);  // < 0: tie
     *inv_sin = fsqrt(dd * h);                                        // 1 / sin(ray, axis)
   }
   return par ? in : (e >= 0.0f);

@@ -67,7 +67,8 @@ __device__ __forceinline__ LeafD leaf_d(D4 q0, D4 D0, D4 D1, D4 D2, double u0, d
 // conservative cylinder of leaf q, FP64, in App. A's closest-approach form
 // (d^2 of eq. P:814, t_cpa P:825-833, s P:862-866) with n = w x d, which keeps full
 // precision near tangency (the expanded quadratic would cancel).
-__device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t) {
+__device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t,
+                                           double* t_exit = nullptr) {
   double dd = ddot3(q.d, q.d);
   D4 x0 = dcross(q.t0, q.d), x1 = dcross(q.t1, q.d);
   double m2 = fmax(ddot3(x0, x0), ddot3(x1, x1));
@@ -82,7 +83,9 @@ __device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t
   if (!(d2 <= R * R)) return false;
   D4 md = dcross(mm, q.d);
   double tcpa = -ddot3(md, n) / A;
-  t = tcpa - sqrt((R * R - d2) * dd / A);
+  const double hs = sqrt((R * R - d2) * dd / A);
+  t = tcpa - hs;
+  if (t_exit) *t_exit = tcpa + hs;
   return isfinite(t);
 }
 
@@ -112,7 +115,9 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
                                          const float4 P1, const float4 P2, const float4 P3,
                                          uint32_t start, int depth, uint32_t kind,
                                          uint32_t lo_tag, float t32, int walk, float& t_out,
-                                         float& u_out, uint32_t& n_out, bool& hit) {
+                                         float& u_out, uint32_t& n_out, bool& hit,
+                                         uint32_t& kind_out) {
+  kind_out = kind;
   const D4 c = D4{0.5 * ((double)P0.x + (double)P3.x), 0.5 * ((double)P0.y + (double)P3.y),
                   0.5 * ((double)P0.z + (double)P3.z), 0.0};
   const D4 q0 = dsub(d4of(P0), c);
@@ -144,26 +149,101 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
       if (wn != 0.0) t = ddot3(dsub(pl.p, m), pl.t0) / wn;
     }
     if (kind == FIBER_KIND_LATERAL) {
-      double te;
-      if (leaf_entry(q, m, w, te)) {
-        t = te;
-        int dir = 0;
-        for (int it = 0; it < walk; ++it) {
-          // side of the entry point w.r.t. the leaf's own start / end planes
-          D4 X = dsub(D4{fma(t, w.x, m.x), fma(t, w.y, m.y), fma(t, w.z, m.z), 0.0}, q.p);
-          double side0 = ddot3(X, q.t0);
-          double side1 = ddot3(dsub(X, q.d), q.t1);
-          int step = 0;
-          if (side0 < 0.0 && k > 0 && dir <= 0) step = -1;
-          else if (side1 > 0.0 && k < nleaf - 1 && dir >= 0) step = +1;
-          if (step == 0) break;
-          LeafD qn = leaf_d(q0, D0, D1, D2, (k + step) * inv, (k + step + 1) * inv);
-          double tn;
-          if (!leaf_entry(qn, m, w, tn)) break;
+      // The leaf test of the oracle in FP64 (P:1618 with F1, F2): the infinite cylinder
+      // interval of leaf kk against its own slab and [0, t_max); t* = max(c0, lo).
+      const uint32_t sh = FIBER_MAX_DEPTH - depth;
+      auto test = [&](int64_t kk, LeafD& qq, double& ts, uint32_t& lu, bool& lateral) {
+        qq = leaf_d(q0, D0, D1, D2, kk * inv, (kk + 1) * inv);
+        double c0, c1;
+        if (!leaf_entry(qq, m, w, c0, &c1)) return false;
+        double lo = 0.0, hi = (double)ray0.w;
+        lu = TAG_ORIGIN;
+        auto clip = [&](double alpha, double beta, uint32_t uu) {  // alpha + beta t >= 0
+          if (beta > 0.0) {
+            double x = -alpha / beta;
+            if (x > lo) lo = x, lu = uu;
+          } else if (beta < 0.0) {
+            hi = fmin(hi, -alpha / beta);
+          } else if (alpha < 0.0) {
+            lo = INFINITY;
+          }
+        };
+        const D4 mp = dsub(m, qq.p);
+        clip(ddot3(mp, qq.t0), ddot3(w, qq.t0), (uint32_t)kk << sh);
+        clip(-ddot3(dsub(mp, qq.d), qq.t1), -ddot3(w, qq.t1), (uint32_t)(kk + 1) << sh);
+        lateral = c0 >= lo;
+        ts = fmax(c0, lo);
+        return (c1 >= lo) && (c0 <= hi) && (lo <= hi) && (ts < (double)ray0.w);
+      };
+      double ts;
+      uint32_t lu;
+      bool lat;
+      bool ok = test(k, q, ts, lu, lat);
+      int dir = 0;
+      for (int it = 0; it < walk; ++it) {
+        LeafD qn;
+        double tn;
+        uint32_t ln;
+        bool latn;
+        if (ok) {
+          if (lat || lu == TAG_ORIGIN) break;  // a lateral entry inside the own slab: first
+          // entered through a crop plane: the leaf across that plane may be entered earlier
+          const int step = (lu == ((uint32_t)k << sh)) ? -1 : +1;
+          if (k + step < 0 || k + step >= nleaf) break;
+          if (!test(k + step, qn, tn, ln, latn) || !(tn < ts)) break;
           k += step;
+        } else {
+          // the FP32 leaf is off (below the crop level): walk towards the cylinder entry
+          double c0;
+          if (!leaf_entry(q, m, w, c0)) break;
+          D4 X = dsub(D4{fma(c0, w.x, m.x), fma(c0, w.y, m.y), fma(c0, w.z, m.z), 0.0}, q.p);
+          int step = 0;
+          if (ddot3(X, q.t0) < 0.0 && k > 0 && dir <= 0) step = -1;
+          else if (ddot3(dsub(X, q.d), q.t1) > 0.0 && k < nleaf - 1 && dir >= 0) step = +1;
+          if (step == 0) break;
           dir = step;
-          q = qn;
-          t = tn;
+          k += step;
+          ok = test(k, qn, tn, ln, latn);
+          if (!ok) {  // keep walking from the new leaf's geometry
+            q = qn;
+            continue;
+          }
+        }
+        q = qn;
+        ts = tn;
+        lu = ln;
+        lat = latn;
+        ok = true;
+      }
+      if (!ok) {
+        if (walk == 0) {  // an exact leaf that fails only by rounding: keep the FP32 entry
+          double c0;
+          if (leaf_entry(q, m, w, c0)) ts = c0, lat = true, ok = true;
+        }
+        if (!ok) {  // no leaf holds an entry: not a hit of the fiber
+          hit = false;
+          t_out = INFINITY;
+          u_out = 0.0f;
+          n_out = 0u;
+          return;
+        }
+      }
+      t = ts;
+      if (!lat) {  // entry through a crop plane (WEDGE; the caps at u = 0 and u = 1)
+        if (lu == TAG_ORIGIN) kind = FIBER_KIND_WEDGE;
+        else if (lu == 0u) kind = FIBER_KIND_CAP0;
+        else if (lu == (1u << FIBER_MAX_DEPTH)) kind = FIBER_KIND_CAP1;
+        else kind = FIBER_KIND_WEDGE;
+        kind_out = kind;
+        if (kind == FIBER_KIND_CAP0 || kind == FIBER_KIND_CAP1) {  // cap normal
+          const bool c0k = kind == FIBER_KIND_CAP0;
+          n = c0k ? dscale(-1.0, D0) : D2;
+          u = c0k ? 0.0 : 1.0;
+          hit = t < (double)ray0.w;
+          t_out = hit ? (float)t : INFINITY;
+          u_out = hit ? (float)u : 0.0f;
+          n_out = hit ? encode_oct32(n.x, n.y, n.z) : 0u;
+          return;
         }
       }
     }
@@ -236,8 +316,7 @@ struct Params {
   float4* hits;
   unsigned long long* nearest;
   unsigned int* counter;  // slot: [0] K2 pair counter, [1] K3 chunk counter, [2] K2 blocks
-                          // done, [3] K3 blocks done, [4] K4 chunk counter, [5] K4 blocks
-                          // done (all zero at launch)
+                          // done, [3] K3 blocks done (all zero at launch)
 #ifdef FIBER_TRACE
   uint32_t trace_pair;  // test build only: per-iteration records of one pair
   float4* trace;        // [kTraceCap] x 3 float4
@@ -249,10 +328,10 @@ __device__ unsigned int g_trace_n;
 #endif
 
 // Internal flags of records between the kernels (never visible after fiber_intersect
-// returns): a provisional hit for K3, an undecided pair for K4.
+// returns): a provisional hit, and a pair to re-run in FP64; K3 consumes both.
 constexpr uint32_t kProvisional = 1u << 6;
 constexpr uint32_t kUncertain = 1u << 7;
-constexpr uint32_t kExactLeaf = 1u << 27;  // in word y of a provisional record: K4's leaf
+constexpr uint32_t kExactLeaf = 1u << 27;  // in word y of a provisional record: FP64 leaf
 constexpr int kWalk = 48;                  // K3's neighbour-leaf walk range
 
 __device__ __forceinline__ void write_record(const Params& p, uint32_t i, uint32_t ray, float t,
@@ -279,7 +358,7 @@ struct Lane {
   float stmin, stmax;  // interval saved at level kCropLevel (deep backtracks)
   float delta;         // FP32 error scale of the local coordinates: 2^-20 max|coordinate|
   float terr, sterr;   // error bound of the current (saved) interval bounds
-  bool tie;            // a decision was a near-tie: re-run the pair in FP64 (K4)
+  uint32_t tie;        // near-tie decisions seen (bit mask): re-run the pair in FP64 (in K3)
   uint32_t tag, stag, bits, start, size, tests, backtracks;
   uint32_t ncache, cache_top, cache_right;  // parent-cache fill, ring top, near-side bits
 };
@@ -371,7 +450,7 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   const float4 L1 = e.h.L0 + e.h.D0, L3 = e.h.L0 + cur.d, L2 = L3 - e.h.D2;
   auto amax = [](float4 v) { return fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z))); };
   e.delta = 9.5367431640625e-07f * fmaxf(fmaxf(amax(e.h.L0), amax(L1)), fmaxf(amax(L2), amax(L3)));
-  e.terr = e.delta * fmaf(4.0f, kappa, 4.0f);
+  e.terr = e.delta * (1.0f + kappa);
   return true;
 }
 
@@ -386,11 +465,11 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
   bool pass = cyl && (c1 >= L.tmin) && (c0 <= L.tmax) && (L.tmin <= L.tmax);
   // near-ties of the test (R5): the entry/exit parameters carry an error of about
   // delta / sin(ray, axis), the interval bounds L.terr
-  const float tau = L.delta * fmaf(8.0f, inv_sin, 8.0f);
+  const float tau = L.delta * fmaf(2.0f, inv_sin, 2.0f);
   const float tb = tau + L.terr;
-  L.tie |= (tie_e < 0.0f) ||
-           (cyl && ((fabsf(c1 - L.tmin) < tb) | (fabsf(L.tmax - c0) < tb) |
-                    (fabsf(L.tmax - L.tmin) < 2.0f * L.terr)));
+  L.tie |= (tie_e < 0.0f ? 1u : 0u) |
+           ((cyl && ((fabsf(c1 - L.tmin) < tb) | (fabsf(L.tmax - c0) < tb) |
+                     (fabsf(L.tmax - L.tmin) < 2.0f * L.terr))) ? 2u : 0u);
 #ifdef FIBER_TRACE
   if (trace) {
     unsigned k = atomicAdd(&g_trace_n, 1u);
@@ -404,12 +483,12 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
 #endif
   if (!pass) return L.bits == 0u ? ST_MISS : ST_NEED_BT;  // done / backtrack
   if (L.size <= min_size) {  // leaf: first hit terminates
-    L.tie |= fabsf(c0 - L.tmin) < tb;  // the kind decision (F2, F6)
+    L.tie |= fabsf(c0 - L.tmin) < tb ? 4u : 0u;  // the kind decision (F2, F6)
     // below the crop level the leaf index is only known to about (error of c0 along the
     // axis) / (leaf length) = tau |d_z| / |d|^2 leaves; K3 walks up to kWalk of them, so
     // nearly parallel rays that could be further off are re-run in FP64
     if (L.size < kCropMinSize)
-      L.tie |= tau * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d);
+      L.tie |= L.delta * inv_sin * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d) ? 8u : 0u;
     L.c0 = c0;
     return ST_HIT;
   }
@@ -422,8 +501,8 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
     // near-ties of the near-child / both decisions and the error of the updated bound.
     // Below the crop level these decisions only pick among nearly collinear leaves (the
     // FP64 finalisation walks to the right one), so they are not re-run.
-    const float tauP = L.delta * fmaf(4.0f, kP, 4.0f);
-    L.tie |= (fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP);
+    const float tauP = L.delta * (1.0f + kP);
+    L.tie |= ((fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP)) ? 16u : 0u;
     if (L.tmin != tmin_in || L.tmax != tmax_in) L.terr = fmaxf(L.terr, tauP);
   }
   // go_down (lst:bitstring_manipulation P:1516-1528)
@@ -475,7 +554,7 @@ __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
   if (L.size >= kCropMinSize) {
     float kappa;
     slab(L.cur, L.lo0, L.hi0, L.start, L.start + L.size, L.tmin, L.tmax, L.tag, !cached, &kappa);
-    L.terr = L.delta * fmaf(4.0f, kappa, 4.0f) * (cached ? 1.0f : 4.0f);
+    L.terr = L.delta * (1.0f + kappa) * (cached ? 1.0f : 4.0f);
     if (L.size == kCropMinSize) {
       L.stmin = L.tmin;
       L.stmax = L.tmax;
@@ -499,8 +578,8 @@ __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
 // kProvisional).
 __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane& L, int st,
                                          uint32_t badseg) {
-  if (L.tie) {  // decided by a near-tie somewhere: K4 re-runs the pair in FP64
-    p.hits[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(badseg | kUncertain));
+  if (L.tie) {  // decided by a near-tie somewhere: K3 re-runs the pair in FP64
+    p.hits[i] = make_float4(0.0f, __uint_as_float(L.tie), 0.0f, __uint_as_float(badseg | kUncertain));
     return;
   }
   if (st == ST_HIT) {
@@ -546,8 +625,11 @@ __device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
   float t, u;
   uint32_t n_oct;
   bool hit;
-  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, lo_tag, t32, exact_leaf ? 0 : kWalk,
-           t, u, n_oct, hit);
+  // the FP32 leaf is exact down to the crop level; below it (and not re-run in FP64) it is
+  // searched for within kWalk leaves
+  const int walk = (exact_leaf || p.depth <= kCropLevel) ? 0 : kWalk;
+  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, lo_tag, t32, walk, t, u, n_oct, hit,
+           kind);
   if (inside && hit) {
     t = 0.0f;
     kind = FIBER_KIND_LATERAL;
@@ -594,7 +676,7 @@ __device__ __forceinline__ void start_lane(const Prepared& e, Lane& L, HodoRef h
   L.tag = L.stag = e.tag;
   L.delta = e.delta;
   L.terr = L.sterr = e.terr;
-  L.tie = false;
+  L.tie = 0u;
   L.bits = 0;
   L.size = 1u << FIBER_MAX_DEPTH;
   L.start = 0;
@@ -663,9 +745,9 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
 }
 
 // ------------------------------------------------------------------------------------
-// K4, the FP64 re-run of the pairs K2 flagged as decided by a near-tie (R5):
-// scans the records, queues flagged pairs per warp and traverses them 32 at a time in
-// double precision (exact.cuh), leaving a provisional record for K3 or the final miss.
+// The FP64 re-run of a pair K2 flagged as decided by a near-tie (R5): the whole
+// traversal in double precision (exact.cuh), leaving a provisional record (with its exact
+// leaf) or the final miss.  Runs inside K3, queued with the provisional hits.
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void exact_one(const Params& p, uint32_t i) {
   const uint32_t badseg = __float_as_uint(p.hits[i].w) & FIBER_BAD_SEGMENT;
@@ -684,42 +766,6 @@ __device__ __forceinline__ void exact_one(const Params& p, uint32_t i) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) exact_kernel(const Params p) {
-  __shared__ uint32_t s_q[kWarps][kQueue];
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t nq = 0;
-  auto flush = [&](uint32_t take) {
-    if (lane < take) exact_one(p, s_q[wid][lane]);
-    __syncwarp();
-    uint32_t mv = 0;
-    bool has = lane + take < nq;
-    if (has) mv = s_q[wid][lane + take];
-    __syncwarp();
-    if (has) s_q[wid][lane] = mv;
-    nq -= take;
-    __syncwarp();
-  };
-  while (true) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&p.counter[4], 128u);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= p.n_pairs) break;
-    for (uint32_t k = 0; k < 128u; k += 32u) {
-      const uint32_t i = base + k + lane;
-      bool unc = false;
-      if (i < p.n_pairs) unc = (__float_as_uint(p.hits[i].w) & kUncertain) != 0u;
-      unsigned m = __ballot_sync(0xffffffffu, unc);
-      if (unc) s_q[wid][nq + __popc(m & lt)] = i;
-      nq += __popc(m);
-      __syncwarp();
-      if (nq >= 32u) flush(32u);
-    }
-  }
-  while (nq > 0u) flush(min(nq, 32u));
-  release_counter(p.counter, 4, 5);
-}
-
 // ------------------------------------------------------------------------------------
 // K3, the finalisation kernel: scans the records, queues provisional hits per warp and
 // finalises them in FP64 32 at a time (converged).  a7, lst:calc_intersection P:1546-1587.
@@ -733,7 +779,19 @@ __global__ void __launch_bounds__(kThreads, FIBER_K3_MINBLOCKS) finalize_kernel(
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t nq = 0;
   auto flush = [&](uint32_t take) {
-    if (lane < take) finalize_one(p, s_q[wid][lane]);
+    if (lane < take) {
+      const uint32_t i = s_q[wid][lane];
+      bool fin = true;
+      if (__float_as_uint(p.hits[i].w) & kUncertain) {
+#ifdef FIBER_NO_EXACT  // test build: leave flagged pairs marked (flag statistics)
+        fin = false;
+#else
+        exact_one(p, i);  // the FP64 traversal, then finalise if it hit
+        fin = (__float_as_uint(p.hits[i].w) & kProvisional) != 0u;
+#endif
+      }
+      if (fin) finalize_one(p, i);
+    }
     __syncwarp();
     uint32_t mv = 0;
     bool has = lane + take < nq;
@@ -751,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K3_MINBLOCKS) finalize_kernel(
     for (uint32_t k = 0; k < 128u; k += 32u) {
       const uint32_t i = base + k + lane;
       bool prov = false;
-      if (i < p.n_pairs) prov = (__float_as_uint(p.hits[i].w) & kProvisional) != 0u;
+      if (i < p.n_pairs) prov = (__float_as_uint(p.hits[i].w) & (kProvisional | kUncertain)) != 0u;
       unsigned m = __ballot_sync(0xffffffffu, prov);
       if (prov) s_q[wid][nq + __popc(m & lt)] = i;
       nq += __popc(m);
@@ -776,7 +834,7 @@ using namespace fiberx;
 // Per-device launch constants, queried once per process and device (immutable afterwards;
 // a call otherwise spends far longer in these queries than the GPU spends on 1M pairs).
 struct LaunchInfo {
-  int sms, k2_per_sm, k3_per_sm, k4_per_sm;
+  int sms, k2_per_sm, k3_per_sm;
   unsigned int* slots;  // kSlots x 4 work counters, zero between uses
 };
 constexpr int kSlots = 1024;  // calls in flight on one device at a time (any streams)
@@ -798,8 +856,7 @@ static const LaunchInfo* launch_info() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k2_per_sm, intersect_kernel, kThreads,
                                                   kSmemBytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k3_per_sm, finalize_kernel, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k4_per_sm, exact_kernel, kThreads, 0);
-    if (li.k4_per_sm < 1) li.k4_per_sm = 1;
+
     if (li.k2_per_sm < 1) li.k2_per_sm = 1;
     if (li.k3_per_sm < 1) li.k3_per_sm = 1;
     if (cudaMalloc((void**)&li.slots, kSlots * kSlotWords * sizeof(unsigned int)) != cudaSuccess) return nullptr;
@@ -876,15 +933,7 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
     if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
     intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
     rc = check_launch("fiber_intersect (traverse)");
-#ifndef FIBER_NO_EXACT
-    if (rc == FIBER_OK) {  // FP64 re-run of near-tie pairs (part of the traversal stage)
-      int64_t xblocks = (int64_t)li->sms * li->k4_per_sm;
-      int64_t xchunks = (n_pairs + 127) / 128;
-      if (xblocks * kWarps > xchunks) xblocks = (xchunks + kWarps - 1) / kWarps;
-      exact_kernel<<<(unsigned)xblocks, kThreads, 0, st>>>(p);
-      rc = check_launch("fiber_intersect (exact)");
-    }
-#endif
+
   }
   if (rc == FIBER_OK && (stages & STAGE_FINALIZE)) {
     int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
@@ -897,6 +946,18 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   if (scratch) cudaFreeAsync(scratch, st);
   return rc;
 }
+
+#ifdef FIBER_TRACE
+// Test build only: record the K2 iterations of pair `pair` into trace (device
+// float4[3 * 256]) during the next fiber_intersect call.
+extern "C" int fiber_debug_trace(uint32_t pair, void* trace) {
+  g_trace_pair = pair;
+  g_trace_buf = (float4*)trace;
+  unsigned zero = 0;
+  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
+  return FIBER_OK;
+}
+#endif
 
 extern "C" int fiber_traverse(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                               const fiber_pair* pairs, int64_t n_pairs, int max_depth,

@@ -13,7 +13,12 @@ fiber = sys.argv[1] if len(sys.argv) > 1 else "A"
 depth = int(sys.argv[2]) if len(sys.argv) > 2 else 22
 targeted = len(sys.argv) > 3 and sys.argv[3] == "t"
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 1 << 15
-w = gen.config4(n_rays=n, depth=depth) if fiber == "C4" else gen.config2(fiber, n_rays=n, depth=depth, targeted=targeted)
+if fiber == "C4":
+    w = gen.config4(n_rays=n, depth=depth)
+elif fiber == "C3":
+    w = gen.config3(n_rays=n, depth=depth)
+else:
+    w = gen.config2(fiber, n_rays=n, depth=depth, targeted=targeted)
 rays, segs, pairs = fx.to_device(w)
 g = fx.unpack(fx.intersect(rays, segs, pairs, depth))
 o = oracle.intersect(w.rays, w.ctrl, w.radii, w.pairs, depth)

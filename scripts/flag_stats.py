@@ -15,5 +15,10 @@ for name, w in (("C2A", gen.config2("A", n_rays=1 << 18, depth=22)),
                 ("C4", gen.config4(n_rays=1 << 15, depth=22))):
     rays, segs, pairs = fx.to_device(w)
     h = fx.intersect(rays, segs, pairs, w.depth)
-    f = h.cpu().numpy().view(np.uint32)[:, 3]
-    print(name, "flagged", ((f >> 7) & 1).mean(), flush=True)
+    hh = h.cpu().numpy().view(np.uint32)
+    f = hh[:, 3]
+    fl = ((f >> 7) & 1) != 0
+    why = hh[fl, 1]
+    print(name, "flagged", fl.mean(), {b: float(((why >> k) & 1).mean()) for k, b in
+                                        enumerate(["cyl", "ival", "kind", "leafidx", "plane"])},
+          flush=True)

@@ -16,12 +16,15 @@ fiber, depth, mode, idx = sys.argv[1], int(sys.argv[2]), sys.argv[3], int(sys.ar
 n = int(sys.argv[5]) if len(sys.argv) > 5 else 1 << 15
 if fiber == "C4":
     w = gen.config4(n_rays=n, depth=depth)
+elif fiber == "C3":
+    w = gen.config3(n_rays=n, depth=depth)
 else:
     w = gen.config2(fiber, n_rays=n, depth=depth, targeted=(mode == "t"))
 L = fx.lib()
 L.fiber_debug_trace.argtypes = [ctypes.c_uint32, ctypes.c_void_p]
 buf = torch.zeros((256 * 3, 4), dtype=torch.float32, device="cuda")
 L.fiber_debug_trace(idx, buf.data_ptr())
+np.save("gpurun_out/trace_w.npy", np.concatenate([w.rays[int(w.pairs[idx, 0])], w.ctrl[int(w.pairs[idx, 1])].ravel(), w.radii[int(w.pairs[idx, 1])]]))
 rays, segs, pairs = fx.to_device(w)
 g = fx.unpack(fx.intersect(rays, segs, pairs, depth))
 torch.cuda.synchronize()
