@@ -156,10 +156,8 @@ def run_ours(args):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
             if record:
                 ev[0].record(stream)
-            fx.traverse(rays, segs, pairs, D, hits)
-            if record:
-                ev[1].record(stream)
-            fx.finalize(rays, segs, pairs, D, hits)
+            fx.intersect_ex(rays, segs, pairs, D, hits=hits,
+                            event_after_traverse=ev[1] if record else None)
             if record:
                 ev[2].record(stream)
                 ms.append(ev)

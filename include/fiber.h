@@ -11,11 +11,12 @@
  *
  * Conventions for every call:
  *   - Pointers marked "device" are CUDA device pointers owned by the caller.  The library
- *     keeps, per device and per process, only immutable launch constants and a pool of
- *     1024 self-resetting 16-byte work-counter slots (allocated on first use), so at most
- *     1024 calls may be in flight on one device at once; it allocates per call only when
- *     fiber_intersect_nearest is given no hits buffer (stream-ordered scratch).  It is
- *     re-entrant and thread-safe.
+ *     keeps, per device and per process, immutable launch constants, a pool of 1024
+ *     self-resetting work-counter slots (so at most 1024 calls may be in flight on one
+ *     device at once) and a private stream-ordered memory pool from which each
+ *     fiber_intersect call takes 8 bytes per pair of scratch (work lists; 16 more per pair
+ *     when no hits buffer is given) and returns it on the same stream.  It is re-entrant
+ *     and thread-safe.
  *   - Work is enqueued on `cuda_stream` (a cudaStream_t, NULL = legacy default stream) and
  *     the call returns immediately; outputs are valid after that stream synchronises, and
  *     inputs must not change before then.  Kernel faults surface at the next sync.
@@ -142,19 +143,14 @@ int fiber_intersect_nearest(const fiber_ray *rays, int64_t n_rays, const fiber_s
                             const fiber_pair *pairs, int64_t n_pairs, int max_depth,
                             fiber_hit *hits, uint64_t *nearest, void *cuda_stream);
 
-/* The two stages of fiber_intersect, for callers that time or overlap them separately.
- * fiber_traverse runs the FP32 traversal (kernel K2) and leaves, for each hit pair,
- * an internal provisional record in hits[i]; fiber_finalize (kernel K3) turns them into
- * final records (FP64 re-solve, lst:calc_intersection P:1546-1587) and, when `nearest`
- * is not NULL, applies the per-ray nearest-hit epilogue.  Both must be called with the
- * same arguments, in this order, on the same stream; between them hits[] is not valid.
- * fiber_intersect(...) == fiber_traverse(...) + fiber_finalize(..., NULL, ...). */
-int fiber_traverse(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
-                   const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
-                   void *cuda_stream);
-int fiber_finalize(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
-                   const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
-                   uint64_t *nearest, void *cuda_stream);
+/* fiber_intersect / fiber_intersect_nearest in one call (hits or nearest may be NULL, not
+ * both), for callers that time the stages: when event_after_traverse (a cudaEvent_t) is
+ * not NULL it is recorded on the stream between the traversal kernel (K2, SURVEY 8(a)
+ * a2-a6) and the finalisation kernel (K3, a7: FP64 re-runs of near-tie pairs and FP64
+ * re-solves of hits that need them).  Errors as fiber_intersect. */
+int fiber_intersect_ex(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
+                       const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
+                       uint64_t *nearest, void *event_after_traverse, void *cuda_stream);
 
 /* Fill nearest[0..n_rays) with the "no hit" key (all ones). */
 int fiber_nearest_init(uint64_t *nearest, int64_t n_rays, void *cuda_stream);

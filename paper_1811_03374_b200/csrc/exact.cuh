@@ -16,6 +16,30 @@
 namespace fiberx {
 namespace exact {
 
+// Double-precision reciprocal and square root from the MUFU seeds (rcp/rsqrt.approx.f64)
+// refined by two Newton steps: ~1 ulp, and a short dependency chain instead of the IEEE
+// division/sqrt sequences (the FP64 path is latency-bound: a re-run is one lane's chain).
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+__device__ __forceinline__ double div64(double a, double b) {
+  const double r = rcp64(b);
+  const double q = a * r;
+  return fma(r, fma(-b, q, a), q);  // one residual correction
+}
+__device__ __forceinline__ double sqrt64(double x) {
+  if (!(x > 0.0)) return x == 0.0 ? 0.0 : sqrt(x);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
+
 struct V4 {
   double x, y, z, w;
 };
@@ -67,18 +91,18 @@ __device__ __forceinline__ void slab(const Curve& c, double lo0, double hi0, uin
   V4 e = add(c.p, c.d);
   double n1 = dot3(c.t1, e), z1 = c.t1.z;
   if (z0 > 0.0) {
-    double x = n0 / z0;
+    double x = div64(n0, z0);
     if (x > tmin) tmin = x, tag = u0tag;
   } else if (z0 < 0.0) {
-    tmax = fmin(tmax, n0 / z0);
+    tmax = fmin(tmax, div64(n0, z0));
   } else if (n0 > 0.0) {
     tmin = INFINITY;
   }
   if (z1 < 0.0) {
-    double x = n1 / z1;
+    double x = div64(n1, z1);
     if (x > tmin) tmin = x, tag = u1tag;
   } else if (z1 > 0.0) {
-    tmax = fmin(tmax, n1 / z1);
+    tmax = fmin(tmax, div64(n1, z1));
   } else if (n1 < 0.0) {
     tmin = INFINITY;
   }
@@ -89,18 +113,18 @@ __device__ __forceinline__ bool cylinder(const Curve& c, double& c0, double& c1)
   double g = fma(c.d.x, c.d.x, c.d.y * c.d.y);
   double dd = fma(c.d.z, c.d.z, g);
   double m2 = fmax(crossn2(c.t0, c.d), crossn2(c.t1, c.d));
-  double R = sqrt(m2 / dd) + c.p.w + fmax(fmax(0.0, c.t0.w), fmax(c.d.w, c.d.w - c.t1.w));
+  double R = sqrt64(m2 * rcp64(dd)) + c.p.w + fmax(fmax(0.0, c.t0.w), fmax(c.d.w, c.d.w - c.t1.w));
   if (g == 0.0) {
     c0 = -INFINITY;
     c1 = INFINITY;
     return fma(c.p.x, c.p.x, c.p.y * c.p.y) <= R * R;
   }
-  const double ig = 1.0 / g;
+  const double ig = rcp64(g);
   double dxy = fma(c.d.x, c.p.y, -c.d.y * c.p.x);
   double e = fma(-dxy * dxy, ig, R * R);
   if (!(e >= 0.0)) return false;
   double tc = fma(-c.d.z * ig, fma(c.d.x, c.p.x, c.d.y * c.p.y), c.p.z);
-  double s = sqrt(e * dd * ig);
+  double s = sqrt64(e * dd * ig);
   c0 = tc - s;
   c1 = tc + s;
   return true;
@@ -119,12 +143,13 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
   Result res{false, 0, 0, 0, 0, kOrigin, 0, 0, 0.0};
   // frame: o' = o + ts w^ next to the segment, ONB (Duff et al.)
   double wx = ray1.x, wy = ray1.y, wz = ray1.z;
-  const double lw = sqrt(wx * wx + wy * wy + wz * wz);
-  wx /= lw;
-  wy /= lw;
-  wz /= lw;
+  const double lw = sqrt64(wx * wx + wy * wy + wz * wz);
+  const double ilw = rcp64(lw);
+  wx *= ilw;
+  wy *= ilw;
+  wz *= ilw;
   const double sign = copysign(1.0, wz);
-  const double a = -1.0 / (sign + wz), b = wx * wy * a;
+  const double a = -rcp64(sign + wz), b = wx * wy * a;
   const V4 b1 = v4(1.0 + sign * wx * wx * a, sign * b, -sign * wx, 0.0);
   const V4 b2 = v4(b, sign + wy * wy * a, -wy, 0.0);
   const V4 W = v4(wx, wy, wz, 0.0);
@@ -174,7 +199,7 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
       double num = dot3(tcn, S), nz = tcn.z;
       bool right, both;
       if (nz != 0.0) {
-        double tP = num / nz;
+        double tP = div64(num, nz);
         right = (tP > c0) != (nz > 0.0);
         both = (c0 < tP) && (tP < c1);
         if (tP > c0) tmax = fmin(tmax, tP);

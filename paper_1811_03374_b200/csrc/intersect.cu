@@ -73,20 +73,39 @@ __device__ __forceinline__ bool leaf_entry(const LeafD& q, D4 m, D4 w, double& t
   D4 x0 = dcross(q.t0, q.d), x1 = dcross(q.t1, q.d);
   double m2 = fmax(ddot3(x0, x0), ddot3(x1, x1));
   double maxr = q.p.w + fmax(fmax(0.0, q.t0.w), fmax(q.d.w, q.d.w - q.t1.w));
-  double R = sqrt(m2 / dd) + maxr;
+  double R = exact::sqrt64(m2 * exact::rcp64(dd)) + maxr;
   D4 mm = dsub(m, q.p);
   D4 n = dcross(w, q.d);            // |n|^2 = |w x d|^2
   double A = ddot3(n, n);
   if (!(A > 0.0)) return false;
   double mn = ddot3(mm, n);
-  double d2 = mn * mn / A;          // squared line-line distance (eq. P:814)
+  const double iA = exact::rcp64(A);
+  double d2 = mn * mn * iA;         // squared line-line distance (eq. P:814)
   if (!(d2 <= R * R)) return false;
   D4 md = dcross(mm, q.d);
-  double tcpa = -ddot3(md, n) / A;
-  const double hs = sqrt((R * R - d2) * dd / A);
+  double tcpa = -ddot3(md, n) * iA;
+  const double hs = exact::sqrt64((R * R - d2) * dd * iA);
   t = tcpa - hs;
   if (t_exit) *t_exit = tcpa + hs;
   return isfinite(t);
+}
+
+// Octahedral snorm16x2 encoding of a (not necessarily unit) FP32 direction.
+__device__ __forceinline__ uint32_t encode_oct_f(float x, float y, float z) {
+  const float l1 = fabsf(x) + fabsf(y) + fabsf(z);
+  if (!(l1 > 0.0f)) return 0u;
+  const float il = frcp(l1);
+  x *= il;
+  y *= il;
+  if (z < 0.0f) {
+    const float ox = (1.0f - fabsf(y)) * copysignf(1.0f, x);
+    const float oy = (1.0f - fabsf(x)) * copysignf(1.0f, y);
+    x = ox;
+    y = oy;
+  }
+  const int ix = __float2int_rn(fminf(1.0f, fmaxf(-1.0f, x)) * 32767.0f);
+  const int iy = __float2int_rn(fminf(1.0f, fmaxf(-1.0f, y)) * 32767.0f);
+  return ((uint32_t)ix & 0xffffu) | (((uint32_t)iy & 0xffffu) << 16);
 }
 
 __device__ __forceinline__ uint32_t encode_oct32(double nx, double ny, double nz) {
@@ -125,7 +144,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
   const D4 m = D4{(double)ray0.x - c.x, (double)ray0.y - c.y, (double)ray0.z - c.z, 0.0};
   const D4 w = D4{ray1.x, ray1.y, ray1.z, 0.0};
   const int64_t nleaf = (int64_t)1 << depth;
-  const double inv = 1.0 / (double)nleaf;
+  const double inv = ldexp(1.0, -depth);
   int64_t k = (int64_t)(start >> (FIBER_MAX_DEPTH - depth));
   double t = (double)t32, u = 0.0;
   D4 n;
@@ -135,7 +154,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
     D4 qp = c0k ? q0 : dsub(d4of(P3), c);
     D4 nn = c0k ? D0 : D2;
     double wn = ddot3(w, nn);
-    if (wn != 0.0) t = ddot3(dsub(qp, m), nn) / wn;
+    if (wn != 0.0) t = exact::div64(ddot3(dsub(qp, m), nn), wn);
     u = c0k ? 0.0 : 1.0;
     n = c0k ? dscale(-1.0, D0) : D2;
   } else {
@@ -146,7 +165,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
       double ul = (double)lo_tag * (1.0 / (double)(1u << FIBER_MAX_DEPTH));
       LeafD pl = leaf_d(q0, D0, D1, D2, ul, ul + inv);  // p = C(ul), t0 = h H(ul, ul)
       double wn = ddot3(w, pl.t0);
-      if (wn != 0.0) t = ddot3(dsub(pl.p, m), pl.t0) / wn;
+      if (wn != 0.0) t = exact::div64(ddot3(dsub(pl.p, m), pl.t0), wn);
     }
     if (kind == FIBER_KIND_LATERAL) {
       // The leaf test of the oracle in FP64 (P:1618 with F1, F2): the infinite cylinder
@@ -160,10 +179,10 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
         lu = TAG_ORIGIN;
         auto clip = [&](double alpha, double beta, uint32_t uu) {  // alpha + beta t >= 0
           if (beta > 0.0) {
-            double x = -alpha / beta;
+            double x = exact::div64(-alpha, beta);
             if (x > lo) lo = x, lu = uu;
           } else if (beta < 0.0) {
-            hi = fmin(hi, -alpha / beta);
+            hi = fmin(hi, exact::div64(-alpha, beta));
           } else if (alpha < 0.0) {
             lo = INFINITY;
           }
@@ -249,7 +268,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
     }
     // u by projection onto the leaf chord, normal from the axis point (F8)
     D4 X = dsub(D4{fma(t, w.x, m.x), fma(t, w.y, m.y), fma(t, w.z, m.z), 0.0}, q.p);
-    double ul = ddot3(X, q.d) / ddot3(q.d, q.d);
+    double ul = exact::div64(ddot3(X, q.d), ddot3(q.d, q.d));
     ul = fmin(1.0, fmax(0.0, ul));
     u = ((double)k + ul) * inv;
     n = D4{fma(-ul, q.d.x, X.x), fma(-ul, q.d.y, X.y), fma(-ul, q.d.z, X.z), 0.0};
@@ -282,12 +301,12 @@ __device__ __forceinline__ bool frame32(const float4 ray0, const float4 ray1, co
   bool ok = isfinite(ray0.x) && isfinite(ray0.y) && isfinite(ray0.z) && isfinite(w.x) &&
             isfinite(w.y) && isfinite(w.z) && !(ray0.w <= 0.0f) && !isnan(ray0.w) && ww > 0.0f;
   float sign = copysignf(1.0f, w.z);
-  float a = -1.0f / (sign + w.z);
+  float a = -frcp(sign + w.z);  // (1 ulp; the basis only needs orthonormality to ~1e-7)
   float b = w.x * w.y * a;
   S.b1 = make_float4(fmaf(sign * w.x * w.x, a, 1.0f), sign * b, -sign * w.x, 0.0f);
   S.b2 = make_float4(b, fmaf(w.y * w.y, a, sign), -w.y, 0.0f);
   c = make_float4(0.5f * (P0.x + P3.x), 0.5f * (P0.y + P3.y), 0.5f * (P0.z + P3.z), 0.0f);
-  S.iww = 1.0f / ww;
+  S.iww = frcp(ww);
   S.ts = fmaf(c.x - ray0.x, w.x, fmaf(c.y - ray0.y, w.y, (c.z - ray0.z) * w.z)) * S.iww;
   // FP64: v = c - o - ts w (exact inputs), rho = (<v,b1>, <v,b2>, <v,w>)
   double ts = S.ts;
@@ -315,8 +334,12 @@ struct Params {
   uint32_t min_size;  // 2^(23 - depth), lst:algorithm
   float4* hits;
   unsigned long long* nearest;
-  unsigned int* counter;  // slot: [0] K2 pair counter, [1] K3 chunk counter, [2] K2 blocks
-                          // done, [3] K3 blocks done (all zero at launch)
+  unsigned int* counter;  // slot: [0] K2 pair counter, [2] K2 blocks done, [4]/[5] list
+                          // appends (re-run / finalise); [0]-[5] are zero at launch and K2's
+                          // last block returns them to zero after copying [4]/[5] to [6]/[7],
+                          // the list lengths K3 reads (so a slot needs no memset between calls)
+  uint32_t* list_exact;   // pairs K2 flagged for the FP64 re-run   [n_pairs]
+  uint32_t* list_fin;     // provisional hits for the FP64 finalise [n_pairs]
 #ifdef FIBER_TRACE
   uint32_t trace_pair;  // test build only: per-iteration records of one pair
   float4* trace;        // [kTraceCap] x 3 float4
@@ -483,7 +506,12 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
 #endif
   if (!pass) return L.bits == 0u ? ST_MISS : ST_NEED_BT;  // done / backtrack
   if (L.size <= min_size) {  // leaf: first hit terminates
-    L.tie |= fabsf(c0 - L.tmin) < tb ? 4u : 0u;  // the kind decision (F2, F6)
+    // the kind decision (F2, F6) matters only where the bound is a global cap or the ray
+    // origin: LATERAL and WEDGE are one class with the same values (R3)
+    const bool cap_bound = L.tag == TAG_ORIGIN || (L.tag == 0u && L.start == 0u) ||
+                           (L.tag == (1u << FIBER_MAX_DEPTH) &&
+                            L.start + L.size == (1u << FIBER_MAX_DEPTH));
+    L.tie |= (cap_bound && fabsf(c0 - L.tmin) < tb) ? 4u : 0u;
     // below the crop level the leaf index is only known to about (error of c0 along the
     // axis) / (leaf length) = tau |d_z| / |d|^2 leaves; K3 walks up to kWalk of them, so
     // nearly parallel rays that could be further off are re-run in FP64
@@ -576,15 +604,19 @@ __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
 // Pair ended with status st: write the miss, or the provisional hit record for K3
 // (z* bits, start | kind << 24 | inside << 26, tag of t_min, counters | bad_segment |
 // kProvisional).
+#ifndef FIBER_FP32_FIN_DEPTH
+#define FIBER_FP32_FIN_DEPTH FIBER_MAX_DEPTH
+#endif
 __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane& L, int st,
-                                         uint32_t badseg) {
+                                         uint32_t badseg, HodoRef hs) {
   if (L.tie) {  // decided by a near-tie somewhere: K3 re-runs the pair in FP64
     p.hits[i] = make_float4(0.0f, __uint_as_float(L.tie), 0.0f, __uint_as_float(badseg | kUncertain));
+    p.list_exact[atomicAdd(&p.counter[4], 1u)] = i;
     return;
   }
   if (st == ST_HIT) {
     // F2: entry into the cropped cylinder; F6: kind from the binding constraint
-    float zs = fmaxf(L.c0, L.tmin);
+    const float zs = fmaxf(L.c0, L.tmin);
     uint32_t kind = FIBER_KIND_LATERAL, inside = 0;
     if (!(L.c0 >= L.tmin)) {
       if (L.tag == TAG_ORIGIN) inside = 1, kind = FIBER_KIND_WEDGE;
@@ -594,9 +626,47 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
       else kind = FIBER_KIND_WEDGE;
     }
     if (zs < L.hi0) {  // strictly before the RAY's t_max
+      // a7 in FP32 when that is accurate enough: the leaf is exact (down to the crop level)
+      // and the FP32 coordinate error is far below the radius (normal error ~ delta / r);
+      // otherwise a provisional record for K3's FP64 re-solve
+      if (!inside && p.depth <= FIBER_FP32_FIN_DEPTH && L.delta < 1.220703125e-4f * L.cur.p.w) {
+        const uint2 pr = __ldg(&p.pairs[i]);
+        const float4 w = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
+        const float sign = copysignf(1.0f, w.z);
+        const float a = -frcp(sign + w.z), b = w.x * w.y * a;
+        const float4 b1 = make_float4(fmaf(sign * w.x * w.x, a, 1.0f), sign * b, -sign * w.x, 0.f);
+        const float4 b2 = make_float4(b, fmaf(w.y * w.y, a, sign), -w.y, 0.f);
+        const float t = zs - L.lo0;  // (z - lo0) / |w|^2, |w| = 1 to FP32 rounding
+        float u, nx, ny, nz;
+        if (kind == FIBER_KIND_CAP0 || kind == FIBER_KIND_CAP1) {
+          const Hodo h = hs.load();
+          const float4 tg = kind == FIBER_KIND_CAP0 ? (-1.0f) * h.D0 : h.D2;
+          u = kind == FIBER_KIND_CAP0 ? 0.0f : 1.0f;
+          nx = tg.x;
+          ny = tg.y;
+          nz = tg.z;
+        } else {  // u by projection onto the leaf chord, normal from the axis point
+          const Delta& c = L.cur;
+          float ul = fmaf(-c.p.x, c.d.x, fmaf(-c.p.y, c.d.y, (zs - c.p.z) * c.d.z)) *
+                     frcp(dot3(c.d, c.d));
+          ul = fminf(1.0f, fmaxf(0.0f, ul));
+          u = fmaf(ul, (float)L.size, (float)L.start) * 1.1920928955078125e-07f;  // 2^-23
+          nx = -fmaf(ul, c.d.x, c.p.x);
+          ny = -fmaf(ul, c.d.y, c.p.y);
+          nz = zs - fmaf(ul, c.d.z, c.p.z);
+        }
+        // back to world coordinates
+        const float wx = fmaf(nx, b1.x, fmaf(ny, b2.x, nz * w.x));
+        const float wy = fmaf(nx, b1.y, fmaf(ny, b2.y, nz * w.y));
+        const float wz = fmaf(nx, b1.z, fmaf(ny, b2.z, nz * w.z));
+        write_record(p, i, pr.x, t, u, encode_oct_f(wx, wy, wz),
+                     FIBER_HIT | (kind << FIBER_KIND_SHIFT) | counter_bits(L) | badseg);
+        return;
+      }
       p.hits[i] = make_float4(zs, __uint_as_float(L.start | (kind << 24) | (inside << 26)),
                               __uint_as_float(L.tag),
                               __uint_as_float(counter_bits(L) | badseg | kProvisional));
+      p.list_fin[atomicAdd(&p.counter[5], 1u)] = i;
       return;
     }
   }
@@ -604,7 +674,7 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
 }
 
 // a7 for one provisional hit (all lanes of the batch run it together, converged).
-__device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
+__device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
   const float4 rec = p.hits[i];
   const uint2 pr = __ldg(&p.pairs[i]);
   const float4 ray0 = __ldg(&p.rays[2 * (int64_t)pr.x]);
@@ -636,19 +706,6 @@ __device__ __forceinline__ void finalize_one(const Params& p, uint32_t i) {
   }
   if (hit) flags |= FIBER_HIT | (kind << FIBER_KIND_SHIFT) | (inside ? FIBER_INSIDE : 0u);
   write_record(p, i, pr.x, t, u, n_oct, flags);
-}
-
-// The last block of a kernel to finish returns its counter slot to zero (all blocks have
-// stopped taking work by then), so the slot is ready for a later call without a memset.
-__device__ __forceinline__ void release_counter(unsigned int* slot, int work, int done) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&slot[done], 1u) == gridDim.x - 1u) {
-      atomicExch(&slot[work], 0u);
-      atomicExch(&slot[done], 0u);
-    }
-  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -735,13 +792,25 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
         if (st == ST_NEED_BT) {
           backtrack(L, hs);  // a5
         } else if (st != ST_RUNNING) {
-          end_pair(p, pair, L, st, badseg);  // a6
+          end_pair(p, pair, L, st, badseg, hs);  // a6-a7
           active = false;
         }
       }
     }
   }
-  release_counter(p.counter, 0, 2);
+  // the last block publishes the list lengths for K3 in slot words 6-7 (stable until the
+  // slot's next use) and returns the slot's working words to zero
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.counter[2], 1u) == gridDim.x - 1u) {
+      __threadfence();
+      p.counter[6] = atomicExch(&p.counter[4], 0u);
+      p.counter[7] = atomicExch(&p.counter[5], 0u);
+      atomicExch(&p.counter[0], 0u);
+      atomicExch(&p.counter[2], 0u);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -749,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
 // traversal in double precision (exact.cuh), leaving a provisional record (with its exact
 // leaf) or the final miss.  Runs inside K3, queued with the provisional hits.
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ void exact_one(const Params& p, uint32_t i) {
+__device__ __noinline__ void exact_one(const Params& p, uint32_t i) {
   const uint32_t badseg = __float_as_uint(p.hits[i].w) & FIBER_BAD_SEGMENT;
   const uint2 pr = __ldg(&p.pairs[i]);
   const float4 ray0 = __ldg(&p.rays[2 * (int64_t)pr.x]);
@@ -770,55 +839,40 @@ __device__ __forceinline__ void exact_one(const Params& p, uint32_t i) {
 // K3, the finalisation kernel: scans the records, queues provisional hits per warp and
 // finalises them in FP64 32 at a time (converged).  a7, lst:calc_intersection P:1546-1587.
 // ------------------------------------------------------------------------------------
+// K3: 128-thread blocks, 3 per SM = 12 warps/SM at <= 170 registers (the FP64 path must not
+// spill: a cold local-memory reload on a latency-bound chain costs more than occupancy).
+constexpr int kK3Threads = 128;
 #ifndef FIBER_K3_MINBLOCKS
-#define FIBER_K3_MINBLOCKS 2
+#define FIBER_K3_MINBLOCKS 3
 #endif
-__global__ void __launch_bounds__(kThreads, FIBER_K3_MINBLOCKS) finalize_kernel(const Params p) {
-  __shared__ uint32_t s_q[kWarps][kQueue];
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t nq = 0;
-  auto flush = [&](uint32_t take) {
-    if (lane < take) {
-      const uint32_t i = s_q[wid][lane];
-      bool fin = true;
-      if (__float_as_uint(p.hits[i].w) & kUncertain) {
-#ifdef FIBER_NO_EXACT  // test build: leave flagged pairs marked (flag statistics)
-        fin = false;
+__global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kernel(const Params p) {
+  // K3 walks the two lists K2 appended to.  The FP64 re-runs are long dependent chains
+  // (latency-, not throughput-bound), so they are dealt round-robin over ALL warps of the
+  // grid first -- item k to warp k mod W, lane k / W -- and a short list runs one lane per
+  // warp with no divergence; a re-run that hits is finalised by the same lane.  No atomics:
+  // both lists are dealt statically from the lengths K2's last block published.
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t n_exact = p.counter[6];
+  const uint32_t n_fin = p.counter[7];
+  const uint32_t W = gridDim.x * (blockDim.x >> 5);
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+#ifndef FIBER_NO_EXACT
+#ifdef FIBER_K3_PACKED  // diagnostic: 32 consecutive re-runs per warp
+  for (uint32_t k = gw * 32u + lane; k < n_exact; k += W * 32u) {
 #else
-        exact_one(p, i);  // the FP64 traversal, then finalise if it hit
-        fin = (__float_as_uint(p.hits[i].w) & kProvisional) != 0u;
+  for (uint32_t k = gw + W * lane; k < n_exact; k += W * 32u) {
 #endif
-      }
-      if (fin) finalize_one(p, i);
-    }
-    __syncwarp();
-    uint32_t mv = 0;
-    bool has = lane + take < nq;
-    if (has) mv = s_q[wid][lane + take];
-    __syncwarp();
-    if (has) s_q[wid][lane] = mv;
-    nq -= take;
-    __syncwarp();
-  };
-  while (true) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&p.counter[1], 128u);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= p.n_pairs) break;
-    for (uint32_t k = 0; k < 128u; k += 32u) {
-      const uint32_t i = base + k + lane;
-      bool prov = false;
-      if (i < p.n_pairs) prov = (__float_as_uint(p.hits[i].w) & (kProvisional | kUncertain)) != 0u;
-      unsigned m = __ballot_sync(0xffffffffu, prov);
-      if (prov) s_q[wid][nq + __popc(m & lt)] = i;
-      nq += __popc(m);
-      __syncwarp();
-      if (nq >= 32u) flush(32u);
-    }
+    const uint32_t i = p.list_exact[k];
+    exact_one(p, i);  // the FP64 traversal, then the finalisation if it hit
+    if (__float_as_uint(p.hits[i].w) & kProvisional) finalize_one(p, i);
   }
-  while (nq > 0u) flush(min(nq, 32u));
-  release_counter(p.counter, 1, 3);
+#endif
+#ifndef FIBER_NO_FIN
+  // 32 provisional hits per warp, chunks dealt from the last warp down so the warps that
+  // hold re-runs get them last
+  for (uint32_t c = W - 1u - gw; c * 32u < n_fin; c += W)
+    if (c * 32u + lane < n_fin) finalize_one(p, p.list_fin[c * 32u + lane]);
+#endif
 }
 
 __global__ void fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
@@ -855,7 +909,7 @@ static const LaunchInfo* launch_info() {
                          (int)kSmemBytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k2_per_sm, intersect_kernel, kThreads,
                                                   kSmemBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k3_per_sm, finalize_kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&li.k3_per_sm, finalize_kernel, kK3Threads, 0);
 
     if (li.k2_per_sm < 1) li.k2_per_sm = 1;
     if (li.k3_per_sm < 1) li.k3_per_sm = 1;
@@ -874,38 +928,58 @@ static uint32_t g_trace_pair = 0xffffffffu;
 static float4* g_trace_buf = nullptr;
 #endif
 
-enum { STAGE_TRAVERSE = 1, STAGE_FINALIZE = 2 };
+// The per-call scratch (two work lists of n_pairs entries, and records when the caller
+// gives none) comes from a private stream-ordered memory pool per device that keeps its
+// memory (no system calls after warm-up, no effect on the application's default pool).
+static cudaMemPool_t scratch_pool(int dev) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pools[dev], &props) != cudaSuccess) return nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  return pools[dev];
+}
 
 static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                             const fiber_pair* pairs, int64_t n_pairs, int max_depth,
-                            fiber_hit* hits, uint64_t* nearest, void* stream, int stages) {
+                            fiber_hit* hits, uint64_t* nearest, void* event_after_traverse,
+                            void* stream) {
   if (n_rays < 0 || n_pairs < 0 || n_rays >= ((int64_t)1 << 32) ||
       n_pairs >= ((int64_t)1 << 32) - 64 || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
     return set_error(FIBER_EINVAL, "fiber_intersect: bad size or depth");
   if (n_pairs > 0 && (!rays || !pairs || (!hits && !nearest) || !segs->p0 || !segs->p1 ||
                       !segs->p2 || !segs->p3 || !segs->flags))
     return set_error(FIBER_EINVAL, "fiber_intersect: NULL pointer");
-  if (stages != (STAGE_TRAVERSE | STAGE_FINALIZE) && !hits)
-    return set_error(FIBER_EINVAL, "fiber_traverse/fiber_finalize: NULL hits");
   int rc = check_device();
   if (rc != FIBER_OK) return rc;
   if (n_pairs == 0) return FIBER_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const LaunchInfo* li = launch_info();
   if (!li) return set_error(FIBER_ECUDA, "fiber_intersect: device query failed");
-  // work counters: a self-resetting slot of the per-device pool (no per-call allocation);
-  // scratch records only when the caller passes no hits buffer (nearest-only calls)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = scratch_pool(dev);
+  // work counters: a self-resetting slot of the per-device pool
   unsigned int* counter = li->slots + kSlotWords * (g_next_slot.fetch_add(1u) % kSlots);
+  const size_t list_bytes = 2 * (size_t)n_pairs * sizeof(uint32_t);
+  const size_t rec_bytes = hits ? 0 : (size_t)n_pairs * sizeof(fiber_hit);
   void* scratch = nullptr;
-  if (!hits) {
-    cudaError_t e = cudaMallocAsync(&scratch, (size_t)n_pairs * sizeof(fiber_hit), st);
-    if (e != cudaSuccess) {
-      char buf[300];
-      snprintf(buf, sizeof(buf), "fiber_intersect: scratch: %s", cudaGetErrorString(e));
-      return set_error(FIBER_ECUDA, buf);
-    }
-    hits = (fiber_hit*)scratch;
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(&scratch, list_bytes + rec_bytes, pool, st)
+                       : cudaErrorMemoryAllocation;
+  if (e != cudaSuccess) {
+    char buf[300];
+    snprintf(buf, sizeof(buf), "fiber_intersect: scratch: %s", cudaGetErrorString(e));
+    return set_error(FIBER_ECUDA, buf);
   }
+  if (!hits) hits = (fiber_hit*)((char*)scratch + list_bytes);
   Params p;
   p.rays = (const float4*)rays;
   p.n_rays = n_rays;
@@ -924,61 +998,31 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   p.trace = g_trace_buf;
 #endif
   p.hits = (float4*)hits;
-  p.nearest = nullptr;  // hits only come out of K3
+  p.nearest = (unsigned long long*)nearest;
   p.counter = counter;
-  rc = FIBER_OK;
-  if (stages & STAGE_TRAVERSE) {
-    int64_t chunks = (n_pairs + 31) / 32;
-    int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
-    if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
-    intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
-    rc = check_launch("fiber_intersect (traverse)");
-
-  }
-  if (rc == FIBER_OK && (stages & STAGE_FINALIZE)) {
-    int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
-    int64_t fchunks = (n_pairs + 127) / 128;
-    if (fblocks * kWarps > fchunks) fblocks = (fchunks + kWarps - 1) / kWarps;
-    p.nearest = (unsigned long long*)nearest;
-    finalize_kernel<<<(unsigned)fblocks, kThreads, 0, st>>>(p);
+  p.list_exact = (uint32_t*)scratch;
+  p.list_fin = (uint32_t*)scratch + n_pairs;
+  int64_t chunks = (n_pairs + 31) / 32;
+  int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
+  if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
+  intersect_kernel<<<(unsigned)blocks, kThreads, kSmemBytes, st>>>(p);
+  rc = check_launch("fiber_intersect (traverse)");
+  if (rc == FIBER_OK && event_after_traverse) cudaEventRecord((cudaEvent_t)event_after_traverse, st);
+  if (rc == FIBER_OK) {
+    const int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
+    finalize_kernel<<<(unsigned)fblocks, kK3Threads, 0, st>>>(p);
     rc = check_launch("fiber_intersect (finalize)");
   }
-  if (scratch) cudaFreeAsync(scratch, st);
+  cudaFreeAsync(scratch, st);
   return rc;
-}
-
-#ifdef FIBER_TRACE
-// Test build only: record the K2 iterations of pair `pair` into trace (device
-// float4[3 * 256]) during the next fiber_intersect call.
-extern "C" int fiber_debug_trace(uint32_t pair, void* trace) {
-  g_trace_pair = pair;
-  g_trace_buf = (float4*)trace;
-  unsigned zero = 0;
-  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
-  return FIBER_OK;
-}
-#endif
-
-extern "C" int fiber_traverse(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
-                              const fiber_pair* pairs, int64_t n_pairs, int max_depth,
-                              fiber_hit* hits, void* cuda_stream) {
-  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nullptr,
-                          cuda_stream, STAGE_TRAVERSE);
-}
-
-extern "C" int fiber_finalize(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
-                              const fiber_pair* pairs, int64_t n_pairs, int max_depth,
-                              fiber_hit* hits, uint64_t* nearest, void* cuda_stream) {
-  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest,
-                          cuda_stream, STAGE_FINALIZE);
 }
 
 extern "C" int fiber_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                                const fiber_pair* pairs, int64_t n_pairs, int max_depth,
                                fiber_hit* hits, void* cuda_stream) {
   if (n_pairs > 0 && !hits) return set_error(FIBER_EINVAL, "fiber_intersect: NULL hits");
-  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nullptr,
-                          cuda_stream, STAGE_TRAVERSE | STAGE_FINALIZE);
+  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nullptr, nullptr,
+                          cuda_stream);
 }
 
 extern "C" int fiber_intersect_nearest(const fiber_ray* rays, int64_t n_rays,
@@ -986,8 +1030,19 @@ extern "C" int fiber_intersect_nearest(const fiber_ray* rays, int64_t n_rays,
                                        int64_t n_pairs, int max_depth, fiber_hit* hits,
                                        uint64_t* nearest, void* cuda_stream) {
   if (n_pairs > 0 && !nearest) return set_error(FIBER_EINVAL, "fiber_intersect_nearest: NULL nearest");
+  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest, nullptr,
+                          cuda_stream);
+}
+
+extern "C" int fiber_intersect_ex(const fiber_ray* rays, int64_t n_rays,
+                                  const fiber_segments* segs, const fiber_pair* pairs,
+                                  int64_t n_pairs, int max_depth, fiber_hit* hits,
+                                  uint64_t* nearest, void* event_after_traverse,
+                                  void* cuda_stream) {
+  if (n_pairs > 0 && !hits && !nearest)
+    return set_error(FIBER_EINVAL, "fiber_intersect_ex: NULL hits and nearest");
   return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest,
-                          cuda_stream, STAGE_TRAVERSE | STAGE_FINALIZE);
+                          event_after_traverse, cuda_stream);
 }
 
 extern "C" int fiber_nearest_init(uint64_t* nearest, int64_t n_rays, void* cuda_stream) {

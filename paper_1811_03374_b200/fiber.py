@@ -29,7 +29,7 @@ BAD_SEGMENT = 1 << 5
 
 # every symbol include/fiber.h declares
 EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
-           "fiber_intersect", "fiber_intersect_nearest", "fiber_traverse", "fiber_finalize",
+           "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_ex",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
 
 
@@ -63,12 +63,11 @@ def lib() -> ctypes.CDLL:
         L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
                                               ctypes.c_int, vp, vp, vp]
         L.fiber_nearest_init.argtypes = [vp, i64, vp]
-        L.fiber_traverse.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp, vp]
-        L.fiber_finalize.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp,
-                                     vp, vp]
+        L.fiber_intersect_ex.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int,
+                                         vp, vp, vp, vp]
         for f in ("fiber_segments_view", "fiber_build_segments", "fiber_intersect",
                   "fiber_intersect_nearest", "fiber_nearest_init", "fiber_abi_version",
-                  "fiber_traverse", "fiber_finalize"):
+                  "fiber_intersect_ex"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -156,26 +155,25 @@ def intersect(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: in
     return hits
 
 
-def traverse(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
-             hits: torch.Tensor, stream=None) -> torch.Tensor:
-    """fiber_traverse (stage 1 of intersect: kernel K2); hits holds provisional records."""
+def intersect_ex(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
+                 hits: torch.Tensor | None = None, nearest: torch.Tensor | None = None,
+                 event_after_traverse=None, stream=None) -> torch.Tensor:
+    """fiber_intersect_ex: intersect (and/or the nearest epilogue); records
+    `event_after_traverse` (a torch.cuda.Event) between the traversal and finalisation
+    kernels."""
     rays = _dev(rays, torch.float32, (8,), "rays")
     pairs = _pairs(pairs)
-    _check(lib().fiber_traverse(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
-                                pairs.data_ptr(), pairs.shape[0], int(depth), hits.data_ptr(),
-                                _stream(stream)), "fiber_traverse")
-    return hits
-
-
-def finalize(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
-             hits: torch.Tensor, nearest: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """fiber_finalize (stage 2 of intersect: kernel K3)."""
-    rays = _dev(rays, torch.float32, (8,), "rays")
-    pairs = _pairs(pairs)
-    _check(lib().fiber_finalize(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
-                                pairs.data_ptr(), pairs.shape[0], int(depth), hits.data_ptr(),
-                                nearest.data_ptr() if nearest is not None else None,
-                                _stream(stream)), "fiber_finalize")
+    if hits is None and nearest is None:
+        hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=rays.device)
+    ev = None
+    if event_after_traverse is not None:
+        event_after_traverse.record(torch.cuda.current_stream() if stream is None else stream)
+        ev = event_after_traverse.cuda_event
+    _check(lib().fiber_intersect_ex(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                    pairs.data_ptr(), pairs.shape[0], int(depth),
+                                    hits.data_ptr() if hits is not None else None,
+                                    nearest.data_ptr() if nearest is not None else None, ev,
+                                    _stream(stream)), "fiber_intersect_ex")
     return hits
 
 

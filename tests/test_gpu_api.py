@@ -26,8 +26,8 @@ def test_stages_equal_intersect_and_deterministic(fx):
     rays, segs, pairs = fx.to_device(w)
     h1 = fx.intersect(rays, segs, pairs, 12)
     h2 = torch.empty_like(h1)
-    fx.traverse(rays, segs, pairs, 12, h2)
-    fx.finalize(rays, segs, pairs, 12, h2)
+    ev = torch.cuda.Event(enable_timing=True)
+    fx.intersect_ex(rays, segs, pairs, 12, hits=h2, event_after_traverse=ev)
     h3 = fx.intersect(rays, segs, pairs, 12)
     torch.cuda.synchronize()
     assert torch.equal(h1.view(torch.int32), h2.view(torch.int32))
