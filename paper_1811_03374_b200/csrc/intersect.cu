@@ -649,8 +649,18 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
           const Delta& c = L.cur;
           float ul = fmaf(-c.p.x, c.d.x, fmaf(-c.p.y, c.d.y, (zs - c.p.z) * c.d.z)) *
                      frcp(dot3(c.d, c.d));
-          ul = fminf(1.0f, fmaxf(0.0f, ul));
-          u = fmaf(ul, (float)L.size, (float)L.start) * 1.1920928955078125e-07f;  // 2^-23
+          // clamped to the leaf down to the crop level, where the leaf is the
+          // oracle's; below it the FP32 leaf may be a few leaves off (bounded by the leaf-index
+          // tie), so the clamp is to the segment: the leaf chord's extension stays within
+          // curvature x offset^2 of the curve, where a leaf clamp would tilt the normal by
+          // offset x leaf length / r
+          if (L.size >= kCropMinSize) {
+            ul = fminf(1.0f, fmaxf(0.0f, ul));
+          } else {
+            const float isz = frcp((float)L.size);
+            ul = fminf((float)((1u << FIBER_MAX_DEPTH) - L.start) * isz, fmaxf(-(float)L.start * isz, ul));
+          }
+          u = fminf(1.0f, fmaxf(0.0f, fmaf(ul, (float)L.size, (float)L.start) * 1.1920928955078125e-07f));  // 2^-23
           nx = -fmaf(ul, c.d.x, c.p.x);
           ny = -fmaf(ul, c.d.y, c.p.y);
           nz = zs - fmaf(ul, c.d.z, c.p.z);

@@ -196,6 +196,33 @@ def config2(fiber: str = "A", n_rays: int = 1 << 20, depth: int = 22, seed: int 
                     radii, pairs, depth, {"seed": seed, "fiber": fiber})
 
 
+def glancing(fiber: str = "A", n_rays: int = 1 << 14, depth: int = 22, radius: float = 0.01,
+             seed: int = 7) -> Workload:
+    """Stress set for the deep-level leaf choice: rays at a small angle theta to the local
+    tangent C'(u) (log-uniform in [1e-3, 0.3] rad), aimed at a point within 1.5 r of C(u)
+    (u ~ U[0.05, 0.95]), origins 2 units back.  Nearly parallel rays cross many leaves per
+    unit of t, so an FP32 leaf choice is least certain there."""
+    rng = _rng(seed)
+    ctrl, radii = single_fiber(fiber, radius)
+    P = ctrl[0].astype(np.float64)
+    u = rng.uniform(0.05, 0.95, n_rays)
+    T = _unit(bezier_tangent(P, u))
+    X = bezier(P, u)
+    n1 = _unit(np.cross(T, rng.normal(size=(n_rays, 3))))
+    n2 = np.cross(T, n1)
+    phi = rng.uniform(0, 2 * np.pi, n_rays)[:, None]
+    rho = 1.5 * radius * np.sqrt(rng.uniform(0, 1, n_rays))[:, None]
+    tgt = X + rho * (np.cos(phi) * n1 + np.sin(phi) * n2)
+    theta = np.exp(rng.uniform(np.log(1e-3), np.log(0.3), n_rays))[:, None]
+    psi = rng.uniform(0, 2 * np.pi, n_rays)[:, None]
+    side = np.where(rng.uniform(0, 1, n_rays) < 0.5, -1.0, 1.0)[:, None]
+    dirs = side * T * np.cos(theta) + np.sin(theta) * (np.cos(psi) * n1 + np.sin(psi) * n2)
+    rays = _pack_rays(tgt - 2.0 * _unit(dirs), dirs)
+    pairs = np.stack([np.arange(n_rays), np.zeros(n_rays)], 1).astype(np.uint32)
+    return Workload(f"glancing:fiber{fiber}:r{radius}:{n_rays}", rays, ctrl, radii, pairs, depth,
+                    {"seed": seed, "fiber": fiber, "radius": radius})
+
+
 # ---------------------------------------------------------------------------------------
 # hair / fur geometry (C3, C4, C5)
 # ---------------------------------------------------------------------------------------
