@@ -143,6 +143,20 @@ int fiber_intersect_nearest(const fiber_ray *rays, int64_t n_rays, const fiber_s
                             const fiber_pair *pairs, int64_t n_pairs, int max_depth,
                             fiber_hit *hits, uint64_t *nearest, void *cuda_stream);
 
+/* Closest hit over candidate lists: fiber_intersect_nearest where each
+ * pair's traversal is bounded by the best hit its ray has so far -- the ray's t_max used as a
+ * running bound: when a pair starts, t_max' = min(ray.tmax, t_best (1 + 2^-19)),
+ * t_best read from nearest[pair.ray].  A bounded traversal returns the unbounded first hit
+ * whenever that lies before the bound, and a miss otherwise, so `nearest` ends bit-identical
+ * to fiber_intersect_nearest's; pairs are only pruned sooner.  The pruning depends on the
+ * order: give each ray's candidates in rounds, nearest candidates first (all rays' first
+ * candidate, then all second candidates, ...).  hits (may be NULL) holds every pair's record,
+ * but only the winning pair's record of each ray is defined (a pair behind the running bound
+ * reads as a miss).  Errors as fiber_intersect_nearest. */
+int fiber_intersect_closest(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
+                            const fiber_pair *pairs, int64_t n_pairs, int max_depth,
+                            fiber_hit *hits, uint64_t *nearest, void *cuda_stream);
+
 /* fiber_intersect / fiber_intersect_nearest in one call (hits or nearest may be NULL, not
  * both), for callers that time the stages: when event_after_traverse (a cudaEvent_t) is
  * not NULL it is recorded on the stream between the traversal kernel (K2, SURVEY 8(a)

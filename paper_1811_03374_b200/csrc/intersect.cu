@@ -20,7 +20,6 @@ namespace fiberx {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kQueue = 64;  // K3 per-warp queue capacity (<= 31 left + 32 new)
 constexpr int kFarCache = 2;  // per-lane cache of pending far children
 constexpr size_t kSmemBytes = (size_t)(4 + 4 * kFarCache) * kThreads * sizeof(float4);
 
@@ -334,6 +333,7 @@ struct Params {
   uint32_t min_size;  // 2^(23 - depth), lst:algorithm
   float4* hits;
   unsigned long long* nearest;
+  int closest;  // bound each pair's t_max by its ray's best hit so far (fiber_intersect_closest)
   unsigned int* counter;  // slot: [0] K2 pair counter, [2] K2 blocks done, [4]/[5] list
                           // appends (re-run / finalise); [0]-[5] are zero at launch and K2's
                           // last block returns them to zero after copying [4]/[5] to [6]/[7],
@@ -461,7 +461,18 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   // ray interval [0, tmax) in local z units: z = (t - ts) |w|^2
   float ww = 1.0f / S.iww;
   e.lo0 = -S.ts * ww;
-  e.hi0 = (ray0.w - S.ts) * ww;
+  float tlim = ray0.w;
+  if (p.closest) {
+    // the ray's t_max as a running bound: the best hit of the
+    // ray so far (read from L2, where the atomicMin of write_record lands), widened by
+    // 2^-19 relative so that hits within FP32 rounding of it still compete for the minimum
+    const unsigned long long key = __ldcg(&p.nearest[pr.x]);
+    if (key != ~0ull) {
+      const float tb = __uint_as_float((uint32_t)(key >> 32));
+      tlim = fminf(tlim, fmaf(tb, 1.9073486328125e-06f, tb) + 1e-30f);
+    }
+  }
+  e.hi0 = (tlim - S.ts) * ww;
   Delta cur;  // conversion {p0,p1,p2,p3} -> {p,d,t0,t1} (3.1 P:372-375)
   cur.p = e.h.L0;
   cur.d = e.h.D0 + e.h.D1 + e.h.D2;
@@ -961,7 +972,7 @@ static cudaMemPool_t scratch_pool(int dev) {
 static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                             const fiber_pair* pairs, int64_t n_pairs, int max_depth,
                             fiber_hit* hits, uint64_t* nearest, void* event_after_traverse,
-                            void* stream) {
+                            void* stream, int closest = 0) {
   if (n_rays < 0 || n_pairs < 0 || n_rays >= ((int64_t)1 << 32) ||
       n_pairs >= ((int64_t)1 << 32) - 64 || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
     return set_error(FIBER_EINVAL, "fiber_intersect: bad size or depth");
@@ -1009,6 +1020,7 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
 #endif
   p.hits = (float4*)hits;
   p.nearest = (unsigned long long*)nearest;
+  p.closest = closest;
   p.counter = counter;
   p.list_exact = (uint32_t*)scratch;
   p.list_fin = (uint32_t*)scratch + n_pairs;
@@ -1042,6 +1054,15 @@ extern "C" int fiber_intersect_nearest(const fiber_ray* rays, int64_t n_rays,
   if (n_pairs > 0 && !nearest) return set_error(FIBER_EINVAL, "fiber_intersect_nearest: NULL nearest");
   return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest, nullptr,
                           cuda_stream);
+}
+
+extern "C" int fiber_intersect_closest(const fiber_ray* rays, int64_t n_rays,
+                                       const fiber_segments* segs, const fiber_pair* pairs,
+                                       int64_t n_pairs, int max_depth, fiber_hit* hits,
+                                       uint64_t* nearest, void* cuda_stream) {
+  if (n_pairs > 0 && !nearest) return set_error(FIBER_EINVAL, "fiber_intersect_closest: NULL nearest");
+  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest, nullptr,
+                          cuda_stream, 1);
 }
 
 extern "C" int fiber_intersect_ex(const fiber_ray* rays, int64_t n_rays,

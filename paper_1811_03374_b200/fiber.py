@@ -29,7 +29,8 @@ BAD_SEGMENT = 1 << 5
 
 # every symbol include/fiber.h declares
 EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
-           "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_ex",
+           "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
+           "fiber_intersect_ex",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
 
 
@@ -62,12 +63,14 @@ def lib() -> ctypes.CDLL:
                                       vp]
         L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
                                               ctypes.c_int, vp, vp, vp]
+        L.fiber_intersect_closest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
+                                              ctypes.c_int, vp, vp, vp]
         L.fiber_nearest_init.argtypes = [vp, i64, vp]
         L.fiber_intersect_ex.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int,
                                          vp, vp, vp, vp]
         for f in ("fiber_segments_view", "fiber_build_segments", "fiber_intersect",
                   "fiber_intersect_nearest", "fiber_nearest_init", "fiber_abi_version",
-                  "fiber_intersect_ex"):
+                  "fiber_intersect_ex", "fiber_intersect_closest"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -190,6 +193,23 @@ def intersect_nearest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, d
                                          hits.data_ptr() if hits is not None else None,
                                          nearest.data_ptr(), _stream(stream)),
            "fiber_intersect_nearest")
+    return nearest
+
+
+def intersect_closest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
+                      nearest: torch.Tensor, hits: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """fiber_intersect_closest: intersect_nearest with each pair bounded by its ray's best hit
+    so far (order the pairs in candidate rounds, nearest first, for the pruning to bite)."""
+    rays = _dev(rays, torch.float32, (8,), "rays")
+    pairs = _pairs(pairs)
+    if nearest.dtype != torch.int64 or nearest.shape != (rays.shape[0],):
+        raise FiberError("nearest must be int64[n_rays]")
+    _check(lib().fiber_intersect_closest(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                         pairs.data_ptr(), pairs.shape[0], int(depth),
+                                         hits.data_ptr() if hits is not None else None,
+                                         nearest.data_ptr(), _stream(stream)),
+           "fiber_intersect_closest")
     return nearest
 
 

@@ -339,6 +339,27 @@ def config3(seed: int = 3374, n_rays: int = 1 << 20, k: int = 16, depth: int = 9
     return Workload("C3:hair100k:16M", rays, ctrl, radii, pairs, depth, {"seed": seed})
 
 
+def candidate_rounds(w: Workload) -> Workload:
+    """The same pairs in candidate rounds for closest-hit queries: each
+    ray's candidates ranked front to back by the distance along the ray to their segment's
+    bounding-box centre, then all rays' rank-0 candidates, all rank-1 candidates, ...  (an
+    ordering of the input; no arithmetic of the method)."""
+    r = w.pairs[:, 0].astype(np.int64)
+    sgi = w.pairs[:, 1].astype(np.int64)
+    centers = 0.5 * (w.ctrl.min(1) + w.ctrl.max(1)).astype(np.float64)
+    o = w.rays[r, 0:3].astype(np.float64)
+    d = w.rays[r, 4:7].astype(np.float64)
+    key = np.einsum("ij,ij->i", centers[sgi] - o, d)
+    by_ray = np.lexsort((key, r))
+    rank = np.empty(w.n_pairs, dtype=np.int64)
+    starts = np.r_[0, np.flatnonzero(np.diff(r[by_ray])) + 1]
+    counts = np.diff(np.r_[starts, w.n_pairs])
+    rank[by_ray] = np.arange(w.n_pairs) - np.repeat(starts, counts)
+    order = np.lexsort((r, rank))
+    return Workload(w.name + "[rounds]", w.rays, w.ctrl, w.radii,
+                    np.ascontiguousarray(w.pairs[order]), w.depth, dict(w.meta, order="rounds"))
+
+
 def config4(seed: int = 3375, n_rays: int = 1 << 24, depth: int = 22) -> Workload:
     """C4: thin fibers (r = 1e-4 chord), one pair per ray, half grazing (xi in +-2e-3),
     half inside (xi in [-1, 0]); D = 22."""
