@@ -92,6 +92,14 @@ typedef struct {
                                                1e-6 of the chord (plane normal undefined)   */
 #define FIBER_SEG_NONFINITE (1u << 6)       /* a NaN/Inf coordinate or radius             */
 #define FIBER_SEG_NEG_RADIUS (1u << 7)      /* a negative radius                           */
+#define FIBER_SEG_QUADRATIC (1u << 8)       /* not an error: a quadratic segment (written by
+                                               fiber_build_segments_quadratic); its planes hold
+                                               p0 = q0, p1 = p2 = q1, p3 = q2 and the kernels
+                                               degree-elevate it exactly (App. B.1)     */
+#define FIBER_SEG_QUAD_CONSTRAINT (1u << 9) /* the quadratic constraint
+                                               <q1 - q0, q1 - q2> <= 0 (App. B.1 eq. P:889) fails */
+/* Bits that make a segment invalid (FIBER_BAD_SEGMENT on its pairs). */
+#define FIBER_SEG_INVALID_MASK (~FIBER_SEG_QUADRATIC)
 
 /* Device-resident segment set, structure of arrays: p[i][s] = (x, y, z, r) of control
  * point i of segment s, one float4 plane per control point (16-B aligned, coalesced
@@ -120,6 +128,19 @@ int fiber_segments_view(void *storage, int64_t n, fiber_segments *out);
  *         FIBER_EDEVICE, FIBER_ECUDA. */
 int fiber_build_segments(const float *ctrl_pts, const float *radii, int64_t n,
                          fiber_segments *segs, void *cuda_stream);
+
+/* Quadratic fibers (the paper evaluates quadratic and cubic fibers,
+ * P:707): like fiber_build_segments for quadratic Bezier segments.  The segment is stored
+ * unrounded (p0 = q0, p1 = p2 = q1, p3 = q2, flag FIBER_SEG_QUADRATIC) and every kernel uses
+ * its exact degree elevation (q0, (q0 + 2 q1)/3, (2 q1 + q2)/3, q2) -- the same curve and
+ * radius function -- so the cubic method applies unchanged (de Casteljau halving commutes
+ * with elevation).  The App. B.1 constraint (eq. P:889) implies the five cubic ones for the
+ * elevated curve; it is checked into FIBER_SEG_QUAD_CONSTRAINT.
+ *   ctrl_pts  device float[n][3][3]  control point positions q0, q1, q2
+ *   radii     device float[n][3]     radius at each control point (quadratic radius)
+ * A segment set is either all cubic or all quadratic.  Errors as fiber_build_segments. */
+int fiber_build_segments_quadratic(const float *ctrl_pts, const float *radii, int64_t n,
+                                   fiber_segments *segs, void *cuda_stream);
 
 /* The hot path (lst:algorithm): for every pair, intersect rays[pair.ray] with
  * segment pair.seg at subdivision depth max_depth and write hits[i].

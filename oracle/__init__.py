@@ -56,6 +56,11 @@ def _load():
                                          ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_double, ctypes.c_double, ctypes.c_int, c_f]
         lib.oracle_intersect.restype = ctypes.c_int
+        lib.oracle_intersect_deg.argtypes = [c_f, ctypes.c_int64, c_f, c_f, ctypes.c_int64,
+                                             ctypes.c_int, c_f, ctypes.c_int64, ctypes.c_int,
+                                             ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_int, c_f]
+        lib.oracle_intersect_deg.restype = ctypes.c_int
         lib.oracle_trace.argtypes = [c_f, c_f, c_f, ctypes.c_int, ctypes.c_double, c_f,
                                      ctypes.c_int, c_f]
         lib.oracle_trace.restype = ctypes.c_int
@@ -85,6 +90,8 @@ def intersect(rays, ctrl, radii, pairs, depth: int, with_eps: bool = True,
 
     rays  f32[n_rays, 8] (ox, oy, oz, tmax, dx, dy, dz, pad)
     ctrl  f32[n_segs, 4, 3]; radii f32[n_segs, 4]; pairs u32[n_pairs, 2] (ray, seg)
+          or quadratic segments ctrl f32[n_segs, 3, 3], radii f32[n_segs, 3]: degree-elevated
+          to cubics in FP64 (oracle.c elevate_quadratic), then the same method
     Returns a dict of numpy arrays: t, u, n (n_pairs x 3), hit (bool), kind, tests,
     backtracks, leaf_u0, leaf_u1, grazing (bool), kind_unstable (bool), eps, and the
     perturbed runs "plus"/"minus" (dicts of t, u, n, kind; kind -1 = miss).
@@ -95,15 +102,17 @@ def intersect(rays, ctrl, radii, pairs, depth: int, with_eps: bool = True,
     radii = np.ascontiguousarray(radii, dtype=np.float32)
     pairs = np.ascontiguousarray(pairs, dtype=np.uint32)
     assert rays.ndim == 2 and rays.shape[1] == 8
-    assert ctrl.shape[1:] == (4, 3) and radii.shape == (ctrl.shape[0], 4)
+    degree = ctrl.shape[1] - 1
+    assert ctrl.shape[1:] in ((4, 3), (3, 3)) and radii.shape == (ctrl.shape[0], degree + 1)
     assert pairs.ndim == 2 and pairs.shape[1] == 2
     n = pairs.shape[0]
     out = np.zeros((n, OREC), dtype=np.float64)
     if nthreads is None:
         nthreads = os.cpu_count() or 1
-    rc = lib.oracle_intersect(_ptr(rays), rays.shape[0], _ptr(ctrl), _ptr(radii), ctrl.shape[0],
-                              _ptr(pairs), n, int(depth), int(bool(with_eps)), float(eps_rel_r),
-                              float(eps_ulps), int(nthreads), _ptr(out))
+    rc = lib.oracle_intersect_deg(_ptr(rays), rays.shape[0], _ptr(ctrl), _ptr(radii),
+                                  ctrl.shape[0], degree, _ptr(pairs), n, int(depth),
+                                  int(bool(with_eps)), float(eps_rel_r), float(eps_ulps),
+                                  int(nthreads), _ptr(out))
     if rc != 0:
         raise ValueError("oracle_intersect: bad arguments")
     return {

@@ -443,11 +443,24 @@ typedef struct {
   const float *ctrl, *radii;
   const uint32_t *pairs;
   int64_t n_rays, n_segs, n_pairs;
-  int D, with_eps;
+  int D, with_eps, degree;
   double eps_rel_r, eps_ulps;
   double *out;
   int64_t begin, end;
 } job;
+
+/* Degree elevation of a quadratic (q0, q1, q2) to the cubic (q0, (q0 + 2 q1)/3,
+ * (2 q1 + q2)/3, q2) -- the same curve (and radius function), so the cubic method applies
+ * unchanged (quadratic fibers, P:707 and App. B.1).  In FP64
+ * from the FP32 inputs.  q: 3 points of 4 doubles (x, y, z, r); P: 4 points of 4. */
+static void elevate_quadratic(const double q[12], double P[16]) {
+  for (int k = 0; k < 4; ++k) {
+    P[k] = q[k];
+    P[4 + k] = (q[k] + 2.0 * q[4 + k]) / 3.0;
+    P[8 + k] = (2.0 * q[4 + k] + q[8 + k]) / 3.0;
+    P[12 + k] = q[8 + k];
+  }
+}
 
 static void load_ctx(octx *c, const job *j, int64_t i) {
   uint32_t ri = j->pairs[2 * i], si = j->pairs[2 * i + 1];
@@ -457,11 +470,22 @@ static void load_ctx(octx *c, const job *j, int64_t i) {
     c->w[k] = ry[4 + k];
   }
   c->tmax = ry[3];
-  const float *cp = j->ctrl + 12 * (int64_t)si;
-  const float *rr = j->radii + 4 * (int64_t)si;
-  for (int p = 0; p < 4; ++p) {
-    for (int k = 0; k < 3; ++k) c->P[4 * p + k] = cp[3 * p + k];
-    c->P[4 * p + 3] = rr[p];
+  if (j->degree == 2) {
+    const float *cp = j->ctrl + 9 * (int64_t)si;
+    const float *rr = j->radii + 3 * (int64_t)si;
+    double q[12];
+    for (int p = 0; p < 3; ++p) {
+      for (int k = 0; k < 3; ++k) q[4 * p + k] = cp[3 * p + k];
+      q[4 * p + 3] = rr[p];
+    }
+    elevate_quadratic(q, c->P);
+  } else {
+    const float *cp = j->ctrl + 12 * (int64_t)si;
+    const float *rr = j->radii + 4 * (int64_t)si;
+    for (int p = 0; p < 4; ++p) {
+      for (int k = 0; k < 3; ++k) c->P[4 * p + k] = cp[3 * p + k];
+      c->P[4 * p + 3] = rr[p];
+    }
   }
   c->D = j->D;
   c->eps = 0.0;
@@ -525,10 +549,12 @@ static void *worker(void *arg) {
 /* rays: f32[n_rays][8] = (ox, oy, oz, tmax, dx, dy, dz, pad); ctrl: f32[n_segs][4][3];
  * radii: f32[n_segs][4]; pairs: u32[n_pairs][2] = (ray, seg); out: f64[n_pairs][OREC].
  * with_eps: also run the +eps / -eps classification.  Returns 0, or -1 on bad args. */
-int oracle_intersect(const float *rays, int64_t n_rays, const float *ctrl, const float *radii,
-                     int64_t n_segs, const uint32_t *pairs, int64_t n_pairs, int depth,
-                     int with_eps, double eps_rel_r, double eps_ulps, int nthreads, double *out) {
-  if (depth < 0 || depth > 23 || n_pairs < 0 || (n_pairs > 0 && (!rays || !ctrl || !radii || !pairs || !out)))
+int oracle_intersect_deg(const float *rays, int64_t n_rays, const float *ctrl,
+                         const float *radii, int64_t n_segs, int degree, const uint32_t *pairs,
+                         int64_t n_pairs, int depth, int with_eps, double eps_rel_r,
+                         double eps_ulps, int nthreads, double *out) {
+  if (depth < 0 || depth > 23 || n_pairs < 0 || (degree != 2 && degree != 3) ||
+      (n_pairs > 0 && (!rays || !ctrl || !radii || !pairs || !out)))
     return -1;
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
@@ -547,6 +573,7 @@ int oracle_intersect(const float *rays, int64_t n_rays, const float *ctrl, const
     j->n_pairs = n_pairs;
     j->D = depth;
     j->with_eps = with_eps;
+    j->degree = degree;
     j->eps_rel_r = eps_rel_r;
     j->eps_ulps = eps_ulps;
     j->out = out;
@@ -561,6 +588,14 @@ int oracle_intersect(const float *rays, int64_t n_rays, const float *ctrl, const
   for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, worker, &jobs[t]);
   for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
   return 0;
+}
+
+/* Cubic segments: ctrl f32[n_segs][4][3], radii f32[n_segs][4]. */
+int oracle_intersect(const float *rays, int64_t n_rays, const float *ctrl, const float *radii,
+                     int64_t n_segs, const uint32_t *pairs, int64_t n_pairs, int depth,
+                     int with_eps, double eps_rel_r, double eps_ulps, int nthreads, double *out) {
+  return oracle_intersect_deg(rays, n_rays, ctrl, radii, n_segs, 3, pairs, n_pairs, depth,
+                              with_eps, eps_rel_r, eps_ulps, nthreads, out);
 }
 
 /* Single pair with an event trace: trace f64[cap][4] rows (level, u0, u1, event)

@@ -139,7 +139,7 @@ struct Result {
 // The whole traversal of one pair in FP64.
 __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1, const float4 P0,
                                         const float4 P1, const float4 P2, const float4 P3,
-                                        int depth) {
+                                        bool quad, int depth) {
   Result res{false, 0, 0, 0, 0, kOrigin, 0, 0, 0.0};
   // frame: o' = o + ts w^ next to the segment, ONB (Duff et al.)
   double wx = ray1.x, wy = ray1.y, wz = ray1.z;
@@ -163,7 +163,10 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
     return v4(dot3(q, b1), dot3(q, b2), dot3(q, W), (double)P.w);
   };
   const V4 L0 = loc(P0), L1 = loc(P1), L2 = loc(P2), L3 = loc(P3);
-  const Hodo64 hc{L0, sub(L1, L0), sub(L2, L1), sub(L3, L2)};
+  // a quadratic (q0, q1, q2) = (P0, P1, P3) is degree-elevated exactly (fiber.h)
+  const Hodo64 hc = quad ? Hodo64{L0, scl(2.0 / 3.0, sub(L1, L0)), scl(1.0 / 3.0, sub(L3, L0)),
+                                  scl(2.0 / 3.0, sub(L3, L1))}
+                         : Hodo64{L0, sub(L1, L0), sub(L2, L1), sub(L3, L2)};
   // ray interval [0, tmax) in local distance units
   const double lo0 = -ts, hi0 = (double)ray0.w * lw - ts;
   Curve cur{L0, sub(L3, L0), hc.D0, hc.D2};

@@ -131,7 +131,7 @@ __device__ __forceinline__ uint32_t encode_oct32(double nx, double ny, double nz
 // the plane that bounds t_min; inside entries keep t = 0.
 __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, const float4 P0,
                                          const float4 P1, const float4 P2, const float4 P3,
-                                         uint32_t start, int depth, uint32_t kind,
+                                         bool quad, uint32_t start, int depth, uint32_t kind,
                                          uint32_t lo_tag, float t32, int walk, float& t_out,
                                          float& u_out, uint32_t& n_out, bool& hit,
                                          uint32_t& kind_out) {
@@ -139,7 +139,13 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
   const D4 c = D4{0.5 * ((double)P0.x + (double)P3.x), 0.5 * ((double)P0.y + (double)P3.y),
                   0.5 * ((double)P0.z + (double)P3.z), 0.0};
   const D4 q0 = dsub(d4of(P0), c);
-  const D4 D0 = dsub(d4of(P1), d4of(P0)), D1 = dsub(d4of(P2), d4of(P1)), D2 = dsub(d4of(P3), d4of(P2));
+  D4 D0 = dsub(d4of(P1), d4of(P0)), D1 = dsub(d4of(P2), d4of(P1)), D2 = dsub(d4of(P3), d4of(P2));
+  if (quad) {  // exact degree elevation of (q0, q1, q2) = (P0, P1, P3), in FP64
+    const D4 a = D0, b = dsub(d4of(P3), d4of(P1));
+    D0 = dscale(2.0 / 3.0, a);
+    D1 = dscale(1.0 / 3.0, dadd(a, b));
+    D2 = dscale(2.0 / 3.0, b);
+  }
   const D4 m = D4{(double)ray0.x - c.x, (double)ray0.y - c.y, (double)ray0.z - c.z, 0.0};
   const D4 w = D4{ray1.x, ray1.y, ray1.z, 0.0};
   const int64_t nleaf = (int64_t)1 << depth;
@@ -443,7 +449,8 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   const float4 ray1 = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
   const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
   const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
-  e.badseg = __ldg(&p.sflags[pr.y]) != 0u ? FIBER_BAD_SEGMENT : 0u;
+  const uint32_t sf = __ldg(&p.sflags[pr.y]);
+  e.badseg = (sf & FIBER_SEG_INVALID_MASK) != 0u ? FIBER_BAD_SEGMENT : 0u;
   e.pair = i;
   Setup32 S;
   float4 rho, c;
@@ -455,9 +462,18 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   // differences are rotated directly, so they keep the relative precision of the inputs
   e.h.L0 = rot(S, w, P0 - c) + rho;
   e.h.L0.w = P0.w;
-  e.h.D0 = rot(S, w, P1 - P0);
-  e.h.D1 = rot(S, w, P2 - P1);
-  e.h.D2 = rot(S, w, P3 - P2);
+  if (sf & FIBER_SEG_QUADRATIC) {
+    // exact degree elevation of (q0, q1, q2) = (P0, P1, P3) from the rotated differences:
+    // Q1 - Q0 = 2/3 (q1 - q0), Q2 - Q1 = 1/3 (q2 - q0), Q3 - Q2 = 2/3 (q2 - q1)
+    const float4 a = rot(S, w, P1 - P0), b = rot(S, w, P3 - P1);
+    e.h.D0 = 0.6666666865348816f * a;
+    e.h.D1 = 0.3333333432674408f * (a + b);
+    e.h.D2 = 0.6666666865348816f * b;
+  } else {
+    e.h.D0 = rot(S, w, P1 - P0);
+    e.h.D1 = rot(S, w, P2 - P1);
+    e.h.D2 = rot(S, w, P3 - P2);
+  }
   // ray interval [0, tmax) in local z units: z = (t - ts) |w|^2
   float ww = 1.0f / S.iww;
   e.lo0 = -S.ts * ww;
@@ -719,7 +735,8 @@ __device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
   // the FP32 leaf is exact down to the crop level; below it (and not re-run in FP64) it is
   // searched for within kWalk leaves
   const int walk = (exact_leaf || p.depth <= kCropLevel) ? 0 : kWalk;
-  finalize(ray0, ray1, P0, P1, P2, P3, start, p.depth, kind, lo_tag, t32, walk, t, u, n_oct, hit,
+  const bool quad = (__ldg(&p.sflags[pr.y]) & FIBER_SEG_QUADRATIC) != 0u;
+  finalize(ray0, ray1, P0, P1, P2, P3, quad, start, p.depth, kind, lo_tag, t32, walk, t, u, n_oct, hit,
            kind);
   if (inside && hit) {
     t = 0.0f;
@@ -846,7 +863,8 @@ __device__ __noinline__ void exact_one(const Params& p, uint32_t i) {
   const float4 ray1 = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
   const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
   const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
-  const exact::Result r = exact::traverse(ray0, ray1, P0, P1, P2, P3, p.depth);
+  const bool quad = (__ldg(&p.sflags[pr.y]) & FIBER_SEG_QUADRATIC) != 0u;
+  const exact::Result r = exact::traverse(ray0, ray1, P0, P1, P2, P3, quad, p.depth);
   const uint32_t cnt = (min(r.backtracks, 255u) << 8) | (min(r.tests, 65535u) << 16);
   if (r.hit) {
     p.hits[i] = make_float4(0.0f, __uint_as_float(r.start | (r.kind << 24) | (r.inside << 26) | kExactLeaf),

@@ -52,7 +52,63 @@ __global__ void __launch_bounds__(256) build_segments_kernel(
   }
 }
 
+// Quadratic segments: validate (App. B.1) and store unrounded; the kernels elevate.
+__global__ void __launch_bounds__(256) build_quadratic_kernel(
+    const float* __restrict__ ctrl, const float* __restrict__ radii, int64_t n,
+    float4* __restrict__ p0, float4* __restrict__ p1, float4* __restrict__ p2,
+    float4* __restrict__ p3, uint32_t* __restrict__ flags) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    double Q[3][3];
+    float r[3];
+    uint32_t f = FIBER_SEG_QUADRATIC;
+    for (int i = 0; i < 3; ++i) {
+      r[i] = radii[3 * s + i];
+      for (int k = 0; k < 3; ++k) {
+        float v = ctrl[9 * s + 3 * i + k];
+        if (!isfinite(v)) f |= FIBER_SEG_NONFINITE;
+        Q[i][k] = v;
+      }
+      if (!isfinite(r[i])) f |= FIBER_SEG_NONFINITE;
+      if (r[i] < 0.0f) f |= FIBER_SEG_NEG_RADIUS;
+    }
+    auto dotd = [&](int a, int b, int c, int d) {  // <Q_a - Q_b, Q_c - Q_d>
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += (Q[a][k] - Q[b][k]) * (Q[c][k] - Q[d][k]);
+      return acc;
+    };
+    if (dotd(1, 0, 1, 2) > 0.0) f |= FIBER_SEG_QUAD_CONSTRAINT;  // eq. P:889
+    double dd = dotd(2, 0, 2, 0), a0 = dotd(1, 0, 1, 0), a1 = dotd(2, 1, 2, 1);
+    if (!(dd > 0.0) || a0 <= 1e-12 * dd || a1 <= 1e-12 * dd) f |= FIBER_SEG_DEGENERATE;
+    const float4 q1 = make_float4((float)Q[1][0], (float)Q[1][1], (float)Q[1][2], r[1]);
+    p0[s] = make_float4((float)Q[0][0], (float)Q[0][1], (float)Q[0][2], r[0]);
+    p1[s] = q1;
+    p2[s] = q1;
+    p3[s] = make_float4((float)Q[2][0], (float)Q[2][1], (float)Q[2][2], r[2]);
+    flags[s] = f;
+  }
+}
+
 }  // namespace
+
+extern "C" int fiber_build_segments_quadratic(const float* ctrl_pts, const float* radii,
+                                              int64_t n, fiber_segments* segs,
+                                              void* cuda_stream) {
+  if (n < 0 || n >= ((int64_t)1 << 32) || !segs || segs->n != n)
+    return set_error(FIBER_EINVAL, "fiber_build_segments_quadratic: bad size or descriptor");
+  if (n > 0 && (!ctrl_pts || !radii || !segs->p0 || !segs->p1 || !segs->p2 || !segs->p3 ||
+                !segs->flags))
+    return set_error(FIBER_EINVAL, "fiber_build_segments_quadratic: NULL pointer");
+  int rc = check_device();
+  if (rc != FIBER_OK) return rc;
+  if (n == 0) return FIBER_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  build_quadratic_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)cuda_stream>>>(
+      ctrl_pts, radii, n, (float4*)segs->p0, (float4*)segs->p1, (float4*)segs->p2,
+      (float4*)segs->p3, segs->flags);
+  return check_launch("fiber_build_segments_quadratic");
+}
 
 extern "C" int fiber_build_segments(const float* ctrl_pts, const float* radii, int64_t n,
                                     fiber_segments* segs, void* cuda_stream) {

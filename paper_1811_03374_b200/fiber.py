@@ -29,6 +29,7 @@ BAD_SEGMENT = 1 << 5
 
 # every symbol include/fiber.h declares
 EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
+           "fiber_build_segments_quadratic",
            "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
            "fiber_intersect_ex",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
@@ -59,6 +60,7 @@ def lib() -> ctypes.CDLL:
         L.fiber_segments_bytes.restype = ctypes.c_size_t
         L.fiber_segments_view.argtypes = [vp, i64, ctypes.POINTER(_Segs)]
         L.fiber_build_segments.argtypes = [vp, vp, i64, ctypes.POINTER(_Segs), vp]
+        L.fiber_build_segments_quadratic.argtypes = [vp, vp, i64, ctypes.POINTER(_Segs), vp]
         L.fiber_intersect.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp,
                                       vp]
         L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
@@ -70,7 +72,8 @@ def lib() -> ctypes.CDLL:
                                          vp, vp, vp, vp]
         for f in ("fiber_segments_view", "fiber_build_segments", "fiber_intersect",
                   "fiber_intersect_nearest", "fiber_nearest_init", "fiber_abi_version",
-                  "fiber_intersect_ex", "fiber_intersect_closest"):
+                  "fiber_intersect_ex", "fiber_intersect_closest",
+                  "fiber_build_segments_quadratic"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -134,6 +137,21 @@ def build_segments(ctrl: torch.Tensor, radii: torch.Tensor, stream=None) -> Segm
     _check(lib().fiber_build_segments(ctrl.data_ptr(), radii.data_ptr(), segs.n,
                                       ctypes.byref(segs.desc), _stream(stream)),
            "fiber_build_segments")
+    segs._keep = (ctrl, radii)
+    return segs
+
+
+def build_segments_quadratic(ctrl: torch.Tensor, radii: torch.Tensor, stream=None) -> Segments:
+    """fiber_build_segments_quadratic: ctrl f32[n,3,3], radii f32[n,3] (CUDA) -> Segments
+    (quadratic Bezier segments, degree-elevated exactly by the kernels)."""
+    ctrl = _dev(ctrl, torch.float32, (3, 3), "ctrl")
+    radii = _dev(radii, torch.float32, (3,), "radii")
+    if radii.shape[0] != ctrl.shape[0]:
+        raise FiberError("ctrl and radii disagree on n")
+    segs = Segments(ctrl.shape[0], ctrl.device)
+    _check(lib().fiber_build_segments_quadratic(ctrl.data_ptr(), radii.data_ptr(), segs.n,
+                                                ctypes.byref(segs.desc), _stream(stream)),
+           "fiber_build_segments_quadratic")
     segs._keep = (ctrl, radii)
     return segs
 
@@ -263,5 +281,5 @@ def to_device(workload, device="cuda"):
     ctrl = torch.from_numpy(np.ascontiguousarray(workload.ctrl)).to(device)
     radii = torch.from_numpy(np.ascontiguousarray(workload.radii)).to(device)
     pairs = torch.from_numpy(np.ascontiguousarray(workload.pairs).view(np.int32)).to(device)
-    segs = build_segments(ctrl, radii)
+    segs = (build_segments_quadratic if ctrl.shape[1] == 3 else build_segments)(ctrl, radii)
     return rays, segs, pairs

@@ -224,6 +224,94 @@ def glancing(fiber: str = "A", n_rays: int = 1 << 14, depth: int = 22, radius: f
 
 
 # ---------------------------------------------------------------------------------------
+# quadratic fibers (the paper evaluates quadratic and cubic fibers)
+# ---------------------------------------------------------------------------------------
+# F_Q: the App. B.1 figure's curve ((0,0), (3.5,1), (4,0)) scaled to unit chord
+# and lifted to 3-D with a small z; <q1-q0, q1-q2> = -0.0444 <= 0 (eq. P:889).
+FIBER_Q = np.array([[0, 0, 0], [.875, .25, .05], [1, 0, 0]], dtype=np.float64)
+
+
+def quadratic_margin(Q: np.ndarray) -> np.ndarray:
+    """-<q1 - q0, q1 - q2> (>= 0 for a valid quadratic, App. B.1 eq. P:889)."""
+    return -np.sum((Q[..., 1, :] - Q[..., 0, :]) * (Q[..., 1, :] - Q[..., 2, :]), -1)
+
+
+def elevate(Q: np.ndarray) -> np.ndarray:
+    """Degree elevation of quadratic Bezier control points [..., 3, k] to cubic [..., 4, k]
+    (textbook identity; used only to build test inputs and pins)."""
+    return np.stack([Q[..., 0, :], (Q[..., 0, :] + 2 * Q[..., 1, :]) / 3,
+                     (2 * Q[..., 1, :] + Q[..., 2, :]) / 3, Q[..., 2, :]], -2)
+
+
+def bezier2(Q: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """Point of quadratic Bezier(s) Q[..., 3, k] at u."""
+    u = np.asarray(u, dtype=np.float64)[..., None]
+    v = 1.0 - u
+    return v * v * Q[..., 0, :] + 2 * u * v * Q[..., 1, :] + u * u * Q[..., 2, :]
+
+
+def bezier2_tangent(Q: np.ndarray, u: np.ndarray) -> np.ndarray:
+    u = np.asarray(u, dtype=np.float64)[..., None]
+    return 2 * ((1 - u) * (Q[..., 1, :] - Q[..., 0, :]) + u * (Q[..., 2, :] - Q[..., 1, :]))
+
+
+def quadratic_fiber(n_rays: int = 1 << 15, depth: int = 9, radius: float = 0.01,
+                    seed: int = 21, targeted: bool = False) -> Workload:
+    """F_Q with C2's ray recipe (origins on a radius-2 sphere about the AABB centre, targets
+    uniform in the AABB dilated by r, or within 2r of the curve)."""
+    rng = _rng(seed)
+    ctrl = FIBER_Q[None].astype(np.float32)
+    radii = np.full((1, 3), radius, dtype=np.float32)
+    X = bezier2(FIBER_Q, np.linspace(0, 1, 1025))
+    lo, hi = X.min(0) - radius, X.max(0) + radius
+    orig = 0.5 * (lo + hi) + 2.0 * _sphere(rng, n_rays)
+    if targeted:
+        u = rng.uniform(0, 1, n_rays)
+        tgt = bezier2(FIBER_Q, u) + 2 * radius * rng.uniform(-1, 1, (n_rays, 3))
+    else:
+        tgt = lo + (hi - lo) * rng.uniform(0, 1, (n_rays, 3))
+    rays = _pack_rays(orig, tgt - orig)
+    pairs = np.stack([np.arange(n_rays), np.zeros(n_rays)], 1).astype(np.uint32)
+    return Workload(f"quadratic:FQ:{'targeted' if targeted else 'random'}{n_rays}", rays, ctrl,
+                    radii, pairs, depth, {"seed": seed})
+
+
+def quadratic_patch(n_segs: int = 4096, n_rays: int = 1 << 15, depth: int = 9,
+                    seed: int = 22) -> Workload:
+    """Random valid quadratic segments (chord 0.1 in the unit cube; q1 = chord midpoint plus
+    an offset inside the ball with diameter q0 q2, which is exactly eq. P:889 by Thales;
+    radius 2e-3..5e-3 per control point), one targeted ray per pair at distance
+    r (1 + xi), xi ~ U[-1.5, 0.5], origins 1 back."""
+    rng = _rng(seed)
+    q0 = rng.uniform(0, 1, (n_segs, 3))
+    q2 = q0 + 0.1 * _sphere(rng, n_segs)
+    mid = 0.5 * (q0 + q2)
+    off = _sphere(rng, n_segs) * (0.05 * 0.95 * rng.uniform(0, 1, (n_segs, 1)) ** (1 / 3))
+    Q = np.stack([q0, mid + off, q2], 1)
+    radii = rng.uniform(2e-3, 5e-3, (n_segs, 3))
+    # the sampled thick-fiber check (P:673-697) on the elevated curve: pull q1 towards the
+    # chord midpoint until it holds (keeps eq. P:889: the ball is convex)
+    for _ in range(8):
+        bad = ~thick_ok(elevate(Q), radii.max(1))
+        if not bad.any():
+            break
+        Q[bad, 1] = 0.5 * Q[bad, 1] + 0.5 * mid[bad]
+    seg = rng.integers(0, n_segs, n_rays)
+    u = rng.uniform(0.02, 0.98, n_rays)
+    w = _sphere(rng, n_rays)
+    C = bezier2(Q[seg], u)
+    T = bezier2_tangent(Q[seg], u)
+    rr = bezier2(radii[seg][..., None], u)[:, 0]
+    nrm = _unit(np.cross(w, T))
+    xi = rng.uniform(-1.5, 0.5, n_rays)
+    tgt = C + (rr * (1 + xi))[:, None] * nrm
+    rays = _pack_rays(tgt - 1.0 * w, w)
+    pairs = np.stack([np.arange(n_rays), seg], 1).astype(np.uint32)
+    return Workload(f"quadratic:patch{n_segs}:{n_rays}", rays, Q.astype(np.float32),
+                    radii.astype(np.float32), pairs, depth, {"seed": seed})
+
+
+# ---------------------------------------------------------------------------------------
 # hair / fur geometry (C3, C4, C5)
 # ---------------------------------------------------------------------------------------
 def _catmull_rom_segments(pts: np.ndarray) -> np.ndarray:
