@@ -98,8 +98,14 @@ typedef struct {
                                                degree-elevate it exactly (App. B.1)     */
 #define FIBER_SEG_QUAD_CONSTRAINT (1u << 9) /* the quadratic constraint
                                                <q1 - q0, q1 - q2> <= 0 (App. B.1 eq. P:889) fails */
+#define FIBER_SEG_THICK (1u << 10)          /* advisory: with the largest radius control point
+                                               r_bar the surface would cross an end plane
+                                               (the conservative test of P:686, "or just")    */
+#define FIBER_SEG_THICK_PARAM (1u << 11)    /* the surface with the cubic radius r(u) crosses
+                                               an end plane: a valid part of
+                                               the fiber would be cropped (thick fiber / cusp) */
 /* Bits that make a segment invalid (FIBER_BAD_SEGMENT on its pairs). */
-#define FIBER_SEG_INVALID_MASK (~FIBER_SEG_QUADRATIC)
+#define FIBER_SEG_INVALID_MASK (~(FIBER_SEG_QUADRATIC | FIBER_SEG_THICK))
 
 /* Device-resident segment set, structure of arrays: p[i][s] = (x, y, z, r) of control
  * point i of segment s, one float4 plane per control point (16-B aligned, coalesced
@@ -141,6 +147,35 @@ int fiber_build_segments(const float *ctrl_pts, const float *radii, int64_t n,
  * A segment set is either all cubic or all quadratic.  Errors as fiber_build_segments. */
 int fiber_build_segments_quadratic(const float *ctrl_pts, const float *radii, int64_t n,
                                    fiber_segments *segs, void *cuda_stream);
+
+/* Input gatekeeper, pre-splitting (3.4 P:609-703: curves that violate the
+ * constraints, and thick or cusp-like regions, "must be subdivided beforehand").  Every
+ * cubic segment is bisected at the parameter midpoint (de Casteljau, FP64) until each piece
+ * satisfies the five constraints and neither of its end planes is crossed by
+ * its surface (the thick-fiber test: r = r(u) if parametric, else the largest radius
+ * control point), or max_level halvings are reached.  Pieces tile [0, 1] in curve order.
+ * Two calls: _count writes offsets (device uint32[n + 1]; offsets[s] = first piece of
+ * segment s, offsets[n] = total, valid after the stream syncs); _write then fills
+ *   out_ctrl  device float[total][4][3], out_radii device float[total][4] (FP32-rounded
+ *             FP64 sub-curves; feed to fiber_build_segments),
+ *   out_src   device uint32[total]  source segment,
+ *   out_u     device float[total][2] (u0, u1) of the piece on its source (dyadic, exact),
+ *   out_valid device uint32[total]  1 if the piece passes, 0 if max_level was reached.
+ * max_level in [0, 16].  Errors: FIBER_EINVAL, FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_presplit_count(const float *ctrl_pts, const float *radii, int64_t n, int max_level,
+                         int parametric, uint32_t *offsets, void *cuda_stream);
+int fiber_presplit_write(const float *ctrl_pts, const float *radii, int64_t n, int max_level,
+                         int parametric, const uint32_t *offsets, float *out_ctrl,
+                         float *out_radii, uint32_t *out_src, float *out_u, uint32_t *out_valid,
+                         void *cuda_stream);
+
+/* u remapping after intersecting pre-split pieces: for every hit record whose pair names
+ * piece k, u <- u0[k] + u (u1[k] - u0[k]) (out_u of fiber_presplit_write); a cap kind at an
+ * inner piece boundary (u0 > 0 for CAP0, u1 < 1 for CAP1) becomes WEDGE (an internal plane).
+ *   hits device fiber_hit[n_pairs] (in/out), pairs device fiber_pair[n_pairs],
+ *   piece_u device float[n_pieces][2].  Errors: FIBER_EINVAL, FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_remap_u(fiber_hit *hits, const fiber_pair *pairs, int64_t n_pairs, const float *piece_u,
+                  int64_t n_pieces, void *cuda_stream);
 
 /* The hot path (lst:algorithm): for every pair, intersect rays[pair.ray] with
  * segment pair.seg at subdivision depth max_depth and write hits[i].

@@ -56,6 +56,10 @@ def _load():
                                          ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_double, ctypes.c_double, ctypes.c_int, c_f]
         lib.oracle_intersect.restype = ctypes.c_int
+        lib.oracle_end_margin.argtypes = [c_f, ctypes.c_int, ctypes.c_int]
+        lib.oracle_end_margin.restype = ctypes.c_double
+        lib.oracle_presplit.argtypes = [c_f, ctypes.c_int, ctypes.c_int, c_f, ctypes.c_int]
+        lib.oracle_presplit.restype = ctypes.c_int
         lib.oracle_intersect_deg.argtypes = [c_f, ctypes.c_int64, c_f, c_f, ctypes.c_int64,
                                              ctypes.c_int, c_f, ctypes.c_int64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -146,6 +150,26 @@ def constraints(P) -> int:
     """Bitmask of violated cubic constraints for positions P f64[4, 3]."""
     P = np.ascontiguousarray(P, dtype=np.float64).reshape(12)
     return int(_load().oracle_constraints(_ptr(P)))
+
+
+def end_margin(P, end: int, parametric: bool = False) -> float:
+    """Thick-fiber / cusp margin of one end: inf over u of rho(u) / r(u); the
+    surface crosses the end plane iff < 1.  P f64[4, 4] (x, y, z, r); end 0 (p0) or 1 (p3);
+    r = the max radius control point, or the cubic radius when parametric."""
+    P = np.ascontiguousarray(P, dtype=np.float64).reshape(16)
+    return float(_load().oracle_end_margin(_ptr(P), int(end), int(bool(parametric))))
+
+
+def presplit(P, max_level: int = 8, parametric: bool = False) -> np.ndarray:
+    """Midpoint pre-splitting until every piece passes the constraints and the thick-fiber
+    test: f64[k, 3] rows (u0, u1, valid) in curve order."""
+    P = np.ascontiguousarray(P, dtype=np.float64).reshape(16)
+    cap = 1 << max_level
+    out = np.zeros((cap, 3))
+    n = _load().oracle_presplit(_ptr(P), int(max_level), int(bool(parametric)), _ptr(out), cap)
+    if n < 0:
+        raise ValueError("oracle_presplit: capacity")
+    return out[:n]
 
 
 def eval_curve(P, u: float, derivative: bool = False) -> np.ndarray:

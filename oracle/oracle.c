@@ -649,3 +649,142 @@ int oracle_constraints(const double P[12]) {
   sub3(p2, p0, a); sub3(p3, p1, b); if (dot3(a, b) < 0) bad |= 16; /* <p2-p0, p3-p1> >= 0 */
   return bad;
 }
+
+/* ------------------------------------------------------------------ */
+/* input gatekeeper: thick-fiber / cusp test and    */
+/* pre-splitting (3.4 P:609-703)                                        */
+/* ------------------------------------------------------------------ */
+
+/* rho(u) for the end plane through p_e with outward unit normal te: the
+ * normal disc at u (centre C(u), normal C'(u)) reaches across the plane exactly when its
+ * radius exceeds
+ *   rho(u) = -<C(u) - p_e, te> / <n^_u, te>,   <n^_u, te> = |C'(u) x te| / |C'(u)|,
+ * n_u = te - <te, t^_u> t^_u being the Gram-Schmidt displacement of P:676-682 (the disc's
+ * point furthest along te is C(u) + r n^_u).  +inf where the disc is parallel to the plane
+ * and the centre is inside; -inf where the centre itself is across. */
+static double end_rho(const double P[16], double u, const double pe[3], const double te[3]) {
+  double c[4], d[4], x[3], m[3];
+  oracle_eval(P, u, c);
+  oracle_eval_derivative(P, u, d);
+  sub3(c, pe, m);
+  cross3(d, te, x);
+  double along = dot3(m, te);
+  double s = norm3(x) / norm3(d);
+  if (s == 0.0) return along <= 0.0 ? INFINITY : -INFINITY;
+  return -along / s;
+}
+
+/* Thick-fiber / cusp margin of one end ("check each fiber only initially in its
+ * two end points"): s* = inf over u in [0, 1) of rho(u) / r(u), with r(u) = the
+ * largest radius control point r_bar ("or just ... r_u <= r_bar") or, parametric = 1,
+ * the cubic radius itself.  The surface crosses the end plane (a valid part would be
+ * cropped) iff s* < 1.  end = 1: the plane through p3 with normal p3 - p2;
+ * end = 0: the plane through p0 with normal p0 - p1 (the reversed curve).
+ * Computed plainly: 4096 uniform samples, 26 samples approaching the end (1 - 2^-j) and the
+ * end limit rho(1) = 1 / curvature(1) = |C'|^3 / |C' x C''| (both numerator and
+ * denominator of rho vanish there), then golden-section refinement around the smallest
+ * sample.  Returns +inf for a straight segment. */
+static double margin_ratio(const double P[16], double u, int parametric, double rbar,
+                           double rho) {
+  double r = rbar;
+  if (parametric) {
+    double c[4];
+    oracle_eval(P, u, c);
+    r = c[3];
+  }
+  return r > 0.0 ? rho / r : INFINITY;
+}
+
+double oracle_end_margin(const double P_in[16], int end, int parametric) {
+  double P[16];
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 4; ++k) P[4 * i + k] = end ? P_in[4 * i + k] : P_in[4 * (3 - i) + k];
+  const double *pe = &P[12];
+  double te[3];
+  sub3(&P[12], &P[8], te);
+  double lt = norm3(te);
+  if (lt == 0.0) return -INFINITY;  /* degenerate end tangent: no plane */
+  for (int k = 0; k < 3; ++k) te[k] /= lt;
+  double rbar = fmax(fmax(P[3], P[7]), fmax(P[11], P[15]));
+  double best = INFINITY, bu = 0.0;
+  const int N = 4096;
+  for (int i = 0; i < N; ++i) {
+    double u = (double)i / N;
+    double v = margin_ratio(P, u, parametric, rbar, end_rho(P, u, pe, te));
+    if (v < best) best = v, bu = u;
+  }
+  for (int j = 1; j <= 26; ++j) {
+    double u = 1.0 - ldexp(1.0, -j);
+    double v = margin_ratio(P, u, parametric, rbar, end_rho(P, u, pe, te));
+    if (v < best) best = v, bu = u;
+  }
+  /* the end limit: C'(1) = 3 (p3 - p2), C''(1) = 6 (p3 - 2 p2 + p1) */
+  {
+    double d1[3], d2[3], x[3];
+    for (int k = 0; k < 3; ++k) {
+      d1[k] = 3.0 * (P[12 + k] - P[8 + k]);
+      d2[k] = 6.0 * (P[12 + k] - 2.0 * P[8 + k] + P[4 + k]);
+    }
+    cross3(d1, d2, x);
+    double l1 = norm3(d1), lx = norm3(x);
+    double rho1 = lx > 0.0 ? l1 * l1 * l1 / lx : INFINITY;
+    double v = margin_ratio(P, 1.0, parametric, rbar, rho1);
+    if (v < best) best = v, bu = 1.0;
+  }
+  if (bu < 1.0 && isfinite(best)) {
+    /* golden-section refinement of the ratio on the bracket around the best sample */
+    double a = fmax(0.0, bu - 1.0 / N), b = fmin(1.0 - ldexp(1.0, -30), bu + 1.0 / N);
+    const double g = 0.5 * (sqrt(5.0) - 1.0);
+    double x1 = b - g * (b - a), x2 = a + g * (b - a);
+    double f1 = margin_ratio(P, x1, parametric, rbar, end_rho(P, x1, pe, te));
+    double f2 = margin_ratio(P, x2, parametric, rbar, end_rho(P, x2, pe, te));
+    for (int it = 0; it < 100; ++it) {
+      if (f1 < f2) {
+        b = x2, x2 = x1, f2 = f1, x1 = b - g * (b - a);
+        f1 = margin_ratio(P, x1, parametric, rbar, end_rho(P, x1, pe, te));
+      } else {
+        a = x1, x1 = x2, f1 = f2, x2 = a + g * (b - a);
+        f2 = margin_ratio(P, x2, parametric, rbar, end_rho(P, x2, pe, te));
+      }
+    }
+    best = fmin(best, fmin(f1, f2));
+  }
+  return best;
+}
+
+/* One segment passes the gatekeeper (3.4 P:609-703): the five constraints hold and neither
+ * end plane is crossed by the surface (margin >= 1 at both ends). */
+static int piece_valid(const double Q[16], int parametric) {
+  double pos[12];
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 3; ++k) pos[3 * i + k] = Q[4 * i + k];
+  if (oracle_constraints(pos)) return 0;
+  return oracle_end_margin(Q, 0, parametric) >= 1.0 && oracle_end_margin(Q, 1, parametric) >= 1.0;
+}
+
+/* Pre-splitting ("must be subdivided beforehand"): bisect at
+ * the parameter midpoint (de Casteljau, via oracle_subcurve) until every piece passes
+ * piece_valid or max_level halvings are reached.  Writes the pieces in curve order as
+ * (u0, u1, valid) triples into out[3 * k ...] (at most cap pieces) and returns their
+ * number (or -1 if cap is too small).  The pieces tile [0, 1]. */
+static int presplit_rec(const double P[16], double u0, double u1, int level, int max_level,
+                        int parametric, double *out, int cap, int n) {
+  if (n < 0) return n;
+  double Q[16];
+  oracle_subcurve(P, u0, u1, Q);
+  int ok = piece_valid(Q, parametric);
+  if (ok || level >= max_level) {
+    if (n >= cap) return -1;
+    out[3 * n] = u0;
+    out[3 * n + 1] = u1;
+    out[3 * n + 2] = ok;
+    return n + 1;
+  }
+  double um = 0.5 * (u0 + u1);
+  n = presplit_rec(P, u0, um, level + 1, max_level, parametric, out, cap, n);
+  return presplit_rec(P, um, u1, level + 1, max_level, parametric, out, cap, n);
+}
+
+int oracle_presplit(const double P[16], int max_level, int parametric, double *out, int cap) {
+  return presplit_rec(P, 0.0, 1.0, 0, max_level, parametric, out, cap, 0);
+}

@@ -8,8 +8,22 @@
 
 #include "fiber.h"
 #include "fiber_internal.h"
+#include "gatekeeper.cuh"
 
 namespace {
+
+// The thick-fiber / cusp test at both ends (gatekeeper.cuh).
+__device__ uint32_t thick_flags(const double P[4][3], const float r[4]) {
+  double Q[4][4];
+  for (int i = 0; i < 4; ++i) {
+    for (int k = 0; k < 3; ++k) Q[i][k] = P[i][k];
+    Q[i][3] = r[i];
+  }
+  uint32_t f = 0;
+  if (fibergk::end_crossed(Q, 0, false) || fibergk::end_crossed(Q, 1, false)) f |= FIBER_SEG_THICK;
+  if (fibergk::end_crossed(Q, 0, true) || fibergk::end_crossed(Q, 1, true)) f |= FIBER_SEG_THICK_PARAM;
+  return f;
+}
 
 __global__ void __launch_bounds__(256) build_segments_kernel(
     const float* __restrict__ ctrl, const float* __restrict__ radii, int64_t n,
@@ -44,6 +58,7 @@ __global__ void __launch_bounds__(256) build_segments_kernel(
     // degenerate chord or end tangent: the cropping plane normal is undefined
     double dd = dotd(3, 0, 3, 0), a0 = dotd(1, 0, 1, 0), a1 = dotd(3, 2, 3, 2);
     if (!(dd > 0.0) || a0 <= 1e-12 * dd || a1 <= 1e-12 * dd) f |= FIBER_SEG_DEGENERATE;
+    if (!(f & (FIBER_SEG_NONFINITE | FIBER_SEG_DEGENERATE))) f |= thick_flags(P, r);
     p0[s] = make_float4((float)P[0][0], (float)P[0][1], (float)P[0][2], r[0]);
     p1[s] = make_float4((float)P[1][0], (float)P[1][1], (float)P[1][2], r[1]);
     p2[s] = make_float4((float)P[2][0], (float)P[2][1], (float)P[2][2], r[2]);
@@ -80,6 +95,22 @@ __global__ void __launch_bounds__(256) build_quadratic_kernel(
     if (dotd(1, 0, 1, 2) > 0.0) f |= FIBER_SEG_QUAD_CONSTRAINT;  // eq. P:889
     double dd = dotd(2, 0, 2, 0), a0 = dotd(1, 0, 1, 0), a1 = dotd(2, 1, 2, 1);
     if (!(dd > 0.0) || a0 <= 1e-12 * dd || a1 <= 1e-12 * dd) f |= FIBER_SEG_DEGENERATE;
+    if (!(f & (FIBER_SEG_NONFINITE | FIBER_SEG_DEGENERATE))) {
+      // the thick-fiber test on the exact elevation
+      double E[4][3];
+      float re[4];
+      for (int k = 0; k < 3; ++k) {
+        E[0][k] = Q[0][k];
+        E[1][k] = (Q[0][k] + 2.0 * Q[1][k]) / 3.0;
+        E[2][k] = (2.0 * Q[1][k] + Q[2][k]) / 3.0;
+        E[3][k] = Q[2][k];
+      }
+      re[0] = r[0];
+      re[1] = (float)(((double)r[0] + 2.0 * r[1]) / 3.0);
+      re[2] = (float)((2.0 * r[1] + (double)r[2]) / 3.0);
+      re[3] = r[2];
+      f |= thick_flags(E, re);
+    }
     const float4 q1 = make_float4((float)Q[1][0], (float)Q[1][1], (float)Q[1][2], r[1]);
     p0[s] = make_float4((float)Q[0][0], (float)Q[0][1], (float)Q[0][2], r[0]);
     p1[s] = q1;

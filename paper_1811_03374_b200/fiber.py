@@ -29,7 +29,8 @@ BAD_SEGMENT = 1 << 5
 
 # every symbol include/fiber.h declares
 EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
-           "fiber_build_segments_quadratic",
+           "fiber_build_segments_quadratic", "fiber_presplit_count", "fiber_presplit_write",
+           "fiber_remap_u",
            "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
            "fiber_intersect_ex",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
@@ -61,6 +62,10 @@ def lib() -> ctypes.CDLL:
         L.fiber_segments_view.argtypes = [vp, i64, ctypes.POINTER(_Segs)]
         L.fiber_build_segments.argtypes = [vp, vp, i64, ctypes.POINTER(_Segs), vp]
         L.fiber_build_segments_quadratic.argtypes = [vp, vp, i64, ctypes.POINTER(_Segs), vp]
+        L.fiber_presplit_count.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int, vp, vp]
+        L.fiber_presplit_write.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int, vp, vp, vp,
+                                           vp, vp, vp, vp]
+        L.fiber_remap_u.argtypes = [vp, vp, i64, vp, i64, vp]
         L.fiber_intersect.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp,
                                       vp]
         L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
@@ -73,7 +78,8 @@ def lib() -> ctypes.CDLL:
         for f in ("fiber_segments_view", "fiber_build_segments", "fiber_intersect",
                   "fiber_intersect_nearest", "fiber_nearest_init", "fiber_abi_version",
                   "fiber_intersect_ex", "fiber_intersect_closest",
-                  "fiber_build_segments_quadratic"):
+                  "fiber_build_segments_quadratic", "fiber_presplit_count",
+                  "fiber_presplit_write", "fiber_remap_u"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -154,6 +160,47 @@ def build_segments_quadratic(ctrl: torch.Tensor, radii: torch.Tensor, stream=Non
            "fiber_build_segments_quadratic")
     segs._keep = (ctrl, radii)
     return segs
+
+
+def presplit(ctrl: torch.Tensor, radii: torch.Tensor, max_level: int = 8,
+             parametric: bool = True, stream=None) -> dict:
+    """fiber_presplit_count / _write: bisect every cubic segment (ctrl f32[n,4,3], radii
+    f32[n,4], CUDA) until its pieces pass the constraints and the thick-fiber test.  Returns
+    dict(ctrl f32[m,4,3], radii f32[m,4], src i32[m], u f32[m,2], valid bool[m],
+    offsets i32[n+1]) on the device (one host sync to size the outputs)."""
+    ctrl = _dev(ctrl, torch.float32, (4, 3), "ctrl")
+    radii = _dev(radii, torch.float32, (4,), "radii")
+    n = ctrl.shape[0]
+    dev = ctrl.device
+    off = torch.zeros(n + 1, dtype=torch.int32, device=dev)
+    _check(lib().fiber_presplit_count(ctrl.data_ptr(), radii.data_ptr(), n, int(max_level),
+                                      int(bool(parametric)), off.data_ptr(), _stream(stream)),
+           "fiber_presplit_count")
+    m = int(off[-1].item())
+    out = {"ctrl": torch.empty((m, 4, 3), dtype=torch.float32, device=dev),
+           "radii": torch.empty((m, 4), dtype=torch.float32, device=dev),
+           "src": torch.empty(m, dtype=torch.int32, device=dev),
+           "u": torch.empty((m, 2), dtype=torch.float32, device=dev),
+           "valid": torch.empty(m, dtype=torch.int32, device=dev), "offsets": off}
+    _check(lib().fiber_presplit_write(ctrl.data_ptr(), radii.data_ptr(), n, int(max_level),
+                                      int(bool(parametric)), off.data_ptr(),
+                                      out["ctrl"].data_ptr(), out["radii"].data_ptr(),
+                                      out["src"].data_ptr(), out["u"].data_ptr(),
+                                      out["valid"].data_ptr(), _stream(stream)),
+           "fiber_presplit_write")
+    out["valid"] = out["valid"] != 0
+    return out
+
+
+def remap_u(hits: torch.Tensor, pairs: torch.Tensor, piece_u: torch.Tensor,
+            stream=None) -> torch.Tensor:
+    """fiber_remap_u: hit u on a pre-split piece -> u on its source segment (in place)."""
+    pairs = _pairs(pairs)
+    piece_u = _dev(piece_u, torch.float32, (2,), "piece_u")
+    _check(lib().fiber_remap_u(hits.data_ptr(), pairs.data_ptr(), pairs.shape[0],
+                               piece_u.data_ptr(), piece_u.shape[0], _stream(stream)),
+           "fiber_remap_u")
+    return hits
 
 
 def _pairs(pairs: torch.Tensor) -> torch.Tensor:

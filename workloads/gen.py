@@ -105,10 +105,15 @@ def constraint_margins(P: np.ndarray) -> np.ndarray:
                      d(p2 - p0, p3 - p2), d(p2 - p0, p3 - p1)], axis=-1)
 
 
-def thick_ok(P: np.ndarray, rbar: np.ndarray, samples: int = 256) -> np.ndarray:
+def thick_ok(P: np.ndarray, rbar: np.ndarray, samples: int = 256,
+             end_samples: int = 0) -> np.ndarray:
     """Sampled stand-in for the thick-fiber test: no point of the normal disc of
-    radius rbar at any sampled u reaches beyond the segment's end planes."""
+    radius rbar at any sampled u reaches beyond the segment's end planes.  end_samples adds
+    samples approaching both ends (u = 2^-j, 1 - 2^-j), where crossings start."""
     u = np.linspace(0.0, 1.0, samples)
+    if end_samples:
+        e = 2.0 ** -np.arange(1, end_samples + 1)
+        u = np.sort(np.r_[u, e, 1.0 - e])
     X = bezier(P[:, None, :, :3], u[None, :])             # [n, s, 3]
     T = _unit(bezier_tangent(P[:, None, :, :3], u[None, :]))
     ok = np.ones(P.shape[0], dtype=bool)
@@ -292,7 +297,7 @@ def quadratic_patch(n_segs: int = 4096, n_rays: int = 1 << 15, depth: int = 9,
     # the sampled thick-fiber check on the elevated curve: pull q1 towards the
     # chord midpoint until it holds (keeps eq. P:889: the ball is convex)
     for _ in range(8):
-        bad = ~thick_ok(elevate(Q), radii.max(1))
+        bad = ~thick_ok(elevate(Q), 1.1 * radii.max(1), end_samples=24)
         if not bad.any():
             break
         Q[bad, 1] = 0.5 * Q[bad, 1] + 0.5 * mid[bad]
@@ -309,6 +314,27 @@ def quadratic_patch(n_segs: int = 4096, n_rays: int = 1 << 15, depth: int = 9,
     pairs = np.stack([np.arange(n_rays), seg], 1).astype(np.uint32)
     return Workload(f"quadratic:patch{n_segs}:{n_rays}", rays, Q.astype(np.float32),
                     radii.astype(np.float32), pairs, depth, {"seed": seed})
+
+
+# ---------------------------------------------------------------------------------------
+# gatekeeper inputs: curves that may violate the constraints / be thick
+# ---------------------------------------------------------------------------------------
+FIG4_LOOP = np.array([[0, 0, 0], [5, 1, 0], [-1, 1, 0], [4, 0, 0]], dtype=np.float64)
+
+
+def gatekeeper_curves(n: int = 2048, seed: int = 31) -> tuple[np.ndarray, np.ndarray]:
+    """Unit-chord cubics with inner control points drawn around the chord (a share of them
+    loops, cusps or overshoots that violate P:614-621) and radii log-uniform in
+    [1e-3, 0.3] (a share thick enough to cross an end plane), per control point +-30%."""
+    rng = _rng(seed)
+    p0 = np.zeros((n, 3))
+    p3 = np.tile([1.0, 0.0, 0.0], (n, 1))
+    spread = np.exp(rng.uniform(np.log(0.05), np.log(1.5), (n, 1)))
+    p1 = np.array([1 / 3, 0, 0]) + spread * rng.normal(size=(n, 3)) * [1, 1, 0.3]
+    p2 = np.array([2 / 3, 0, 0]) + spread * rng.normal(size=(n, 3)) * [1, 1, 0.3]
+    ctrl = np.stack([p0, p1, p2, p3], 1)
+    r = np.exp(rng.uniform(np.log(1e-3), np.log(0.3), (n, 1))) * rng.uniform(0.7, 1.3, (n, 4))
+    return ctrl.astype(np.float32), r.astype(np.float32)
 
 
 # ---------------------------------------------------------------------------------------
