@@ -177,6 +177,39 @@ int fiber_presplit_write(const float *ctrl_pts, const float *radii, int64_t n, i
 int fiber_remap_u(fiber_hit *hits, const fiber_pair *pairs, int64_t n_pairs, const float *piece_u,
                   int64_t n_pieces, void *cuda_stream);
 
+/* Candidate-pair generation (the top-level hierarchy of P:753-759): a
+ * uniform grid over the segments' bounding boxes (control points dilated by the largest
+ * radius control point) and a 3-D DDA per ray that emits every segment whose box
+ * the ray overlaps on [0, tmax), front to back by cell (ascending segment id within a cell).
+ * Conservative: a segment the ray hits is always a candidate (boxes are dilated by 1e-3 of a
+ * cell against FP32 rounding; a segment may appear twice, which does not change a nearest
+ * hit).  The grid is an opaque handle that owns its device memory. */
+typedef struct fiber_grid_s fiber_grid;
+
+/* Build the grid over `segs` (about cells_per_segment x n cells, each axis <= 1024) on the
+ * current device.  Synchronises the stream (the sizes are data-dependent).
+ * Errors: FIBER_EINVAL (n == 0, NULL, cells_per_segment <= 0), FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_grid_create(const fiber_segments *segs, float cells_per_segment, fiber_grid **grid,
+                      void *cuda_stream);
+int fiber_grid_destroy(fiber_grid *grid);
+/* Host-only: cells per axis and the number of (cell, segment) entries. */
+int fiber_grid_info(const fiber_grid *grid, int32_t dims[3], int64_t *n_entries);
+
+/* Pass 1: offsets (device uint32[n_rays + 1]) = exclusive scan of the candidate counts per
+ * ray; *max_count and *total (host) are the largest count and offsets[n_rays].  Synchronises
+ * the stream. */
+int fiber_grid_count(const fiber_grid *grid, const fiber_ray *rays, int64_t n_rays,
+                     uint32_t *offsets, uint32_t *max_count, uint64_t *total, void *cuda_stream);
+
+/* Pass 2: write the total candidate pairs into pairs (device fiber_pair[total]).
+ *   order 0: ray-major (ray r's candidates at offsets[r] .. offsets[r+1], front to back);
+ *   order 1: rounds (every ray's first candidate in ray order, then every second one, ...),
+ *            the order fiber_intersect_closest prunes best with (deterministic).
+ * Errors: FIBER_EINVAL, FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_grid_candidates(const fiber_grid *grid, const fiber_ray *rays, int64_t n_rays,
+                          const uint32_t *offsets, uint32_t max_count, int order,
+                          fiber_pair *pairs, void *cuda_stream);
+
 /* The hot path (lst:algorithm): for every pair, intersect rays[pair.ray] with
  * segment pair.seg at subdivision depth max_depth and write hits[i].
  *   rays      device fiber_ray[n_rays]

@@ -11,8 +11,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "segments.cu", "intersect.cu", "presplit.cu"]
-HEADERS = ["fiber_device.cuh", "fiber_internal.h", "exact.cuh", "gatekeeper.cuh"]
+SOURCES = ["api.cu", "segments.cu", "intersect.cu", "presplit.cu", "grid.cu"]
+HEADERS = ["fiber_device.cuh", "fiber_internal.h", "exact.cuh", "gatekeeper.cuh", "scan.cuh"]
 LIB = os.path.join(HERE, "libfiber.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

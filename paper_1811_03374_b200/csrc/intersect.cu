@@ -1008,7 +1008,8 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   cudaMemPool_t pool = scratch_pool(dev);
   // work counters: a self-resetting slot of the per-device pool
   unsigned int* counter = li->slots + kSlotWords * (g_next_slot.fetch_add(1u) % kSlots);
-  const size_t list_bytes = 2 * (size_t)n_pairs * sizeof(uint32_t);
+  // the lists first, the records (16-B float4 stores) at the next 256-B boundary
+  const size_t list_bytes = (2 * (size_t)n_pairs * sizeof(uint32_t) + 255) & ~(size_t)255;
   const size_t rec_bytes = hits ? 0 : (size_t)n_pairs * sizeof(fiber_hit);
   void* scratch = nullptr;
   cudaError_t e = pool ? cudaMallocFromPoolAsync(&scratch, list_bytes + rec_bytes, pool, st)

@@ -30,7 +30,8 @@ BAD_SEGMENT = 1 << 5
 # every symbol include/fiber.h declares
 EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
            "fiber_build_segments_quadratic", "fiber_presplit_count", "fiber_presplit_write",
-           "fiber_remap_u",
+           "fiber_remap_u", "fiber_grid_create", "fiber_grid_destroy", "fiber_grid_info",
+           "fiber_grid_count", "fiber_grid_candidates",
            "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
            "fiber_intersect_ex",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
@@ -66,6 +67,13 @@ def lib() -> ctypes.CDLL:
         L.fiber_presplit_write.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int, vp, vp, vp,
                                            vp, vp, vp, vp]
         L.fiber_remap_u.argtypes = [vp, vp, i64, vp, i64, vp]
+        L.fiber_grid_create.argtypes = [ctypes.POINTER(_Segs), ctypes.c_float,
+                                        ctypes.POINTER(vp), vp]
+        L.fiber_grid_destroy.argtypes = [vp]
+        L.fiber_grid_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(i64)]
+        L.fiber_grid_count.argtypes = [vp, vp, i64, vp, ctypes.POINTER(ctypes.c_uint32),
+                                       ctypes.POINTER(ctypes.c_uint64), vp]
+        L.fiber_grid_candidates.argtypes = [vp, vp, i64, vp, ctypes.c_uint32, ctypes.c_int, vp, vp]
         L.fiber_intersect.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp,
                                       vp]
         L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
@@ -79,7 +87,9 @@ def lib() -> ctypes.CDLL:
                   "fiber_intersect_nearest", "fiber_nearest_init", "fiber_abi_version",
                   "fiber_intersect_ex", "fiber_intersect_closest",
                   "fiber_build_segments_quadratic", "fiber_presplit_count",
-                  "fiber_presplit_write", "fiber_remap_u"):
+                  "fiber_presplit_write", "fiber_remap_u", "fiber_grid_create",
+                  "fiber_grid_destroy", "fiber_grid_info", "fiber_grid_count",
+                  "fiber_grid_candidates"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -201,6 +211,44 @@ def remap_u(hits: torch.Tensor, pairs: torch.Tensor, piece_u: torch.Tensor,
                                piece_u.data_ptr(), piece_u.shape[0], _stream(stream)),
            "fiber_remap_u")
     return hits
+
+
+class Grid:
+    """Candidate-pair generator (fiber_grid_*): a uniform grid over a segment set; a DDA per
+    ray emits the segments whose bounding boxes it overlaps, front to back."""
+
+    def __init__(self, segs: Segments, cells_per_segment: float = 1.0, stream=None):
+        h = ctypes.c_void_p()
+        _check(lib().fiber_grid_create(ctypes.byref(segs.desc), float(cells_per_segment),
+                                       ctypes.byref(h), _stream(stream)), "fiber_grid_create")
+        self._h = h
+        self._segs = segs
+        dims = (ctypes.c_int32 * 3)()
+        ne = ctypes.c_int64()
+        _check(lib().fiber_grid_info(self._h, dims, ctypes.byref(ne)), "fiber_grid_info")
+        self.dims = tuple(dims)
+        self.n_entries = ne.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.fiber_grid_destroy(self._h)
+            self._h = None
+
+    def candidates(self, rays: torch.Tensor, order: str = "rounds", stream=None):
+        """-> (pairs i32[m, 2], offsets i32[n_rays + 1] of the ray-major counts)."""
+        rays = _dev(rays, torch.float32, (8,), "rays")
+        n = rays.shape[0]
+        off = torch.empty(n + 1, dtype=torch.int32, device=rays.device)
+        mx = ctypes.c_uint32()
+        tot = ctypes.c_uint64()
+        _check(lib().fiber_grid_count(self._h, rays.data_ptr(), n, off.data_ptr(),
+                                      ctypes.byref(mx), ctypes.byref(tot), _stream(stream)),
+               "fiber_grid_count")
+        pairs = torch.empty((max(int(tot.value), 1), 2), dtype=torch.int32, device=rays.device)
+        _check(lib().fiber_grid_candidates(self._h, rays.data_ptr(), n, off.data_ptr(), mx.value,
+                                           {"ray": 0, "rounds": 1}[order], pairs.data_ptr(),
+                                           _stream(stream)), "fiber_grid_candidates")
+        return pairs[:int(tot.value)], off
 
 
 def _pairs(pairs: torch.Tensor) -> torch.Tensor:

@@ -68,6 +68,12 @@ def test_nearest_epilogue_matches_host_mirror(fx):
     fx.nearest_init(near2)
     fx.intersect_nearest(rays, segs, pairs, 8, near2)
     assert torch.equal(near, near2)
+    # an odd pair count without a hits buffer (the scratch records must stay 16-B aligned)
+    near3 = torch.empty_like(near)
+    fx.nearest_init(near3)
+    fx.intersect_nearest(rays, segs, pairs[:-1], 8, near3)
+    exp3 = fxd.nearest_keys_host(g["t"][:-1], g["hit"][:-1], pairs_np[:-1], n_rays)
+    assert np.array_equal(near3.cpu().numpy(), exp3)
 
 
 def test_segment_flags_and_planes(fx):
