@@ -794,10 +794,17 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
   const uint32_t min_size = p.min_size;
   Lane L;
   uint32_t pair = 0, badseg = 0;
+  int ended = ST_RUNNING;  // a finished pair whose record is not written yet
   bool active = false, drained = false;
   while (true) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (!drained && (__popc(idle) >= (int)kRefill || idle == 0xffffffffu)) {
+      // a6-a7 for the lanes that finished since the last refill, together (the lane keeps
+      // its state until then), so the record writer runs at the refill's SIMT width
+      if (ended != ST_RUNNING) {
+        end_pair(p, pair, L, ended, badseg, hs);
+        ended = ST_RUNNING;
+      }
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&p.counter[0], (uint32_t)__popc(idle));
       base = __shfl_sync(0xffffffffu, base, 0);
@@ -830,12 +837,13 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
         if (st == ST_NEED_BT) {
           backtrack(L, hs);  // a5
         } else if (st != ST_RUNNING) {
-          end_pair(p, pair, L, st, badseg, hs);  // a6-a7
+          ended = st;  // a6-a7 at the next refill (or the exit)
           active = false;
         }
       }
     }
   }
+  if (ended != ST_RUNNING) end_pair(p, pair, L, ended, badseg, hs);
   // the last block publishes the list lengths for K3 in slot words 6-7 (stable until the
   // slot's next use) and returns the slot's working words to zero
   __syncthreads();
