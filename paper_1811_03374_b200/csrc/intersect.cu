@@ -21,7 +21,8 @@ namespace fiberx {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kFarCache = 2;  // per-lane cache of pending far children
-constexpr size_t kSmemBytes = (size_t)(4 + 4 * kFarCache) * kThreads * sizeof(float4);
+constexpr int kRingF4 = 5;  // a ring entry: the parent's Delta (4 float4) + its interval
+constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache) * kThreads * sizeof(float4);
 
 // ------------------------------------------------------------------------------------
 // a7: FP64 finalisation (lst:calc_intersection P:1546-1587 with F2, F6, F8)
@@ -400,19 +401,21 @@ enum : int { ST_RUNNING = 0, ST_MISS = 1, ST_HIT = 2, ST_NEED_BT = 3 };
 struct HodoRef {
   float4* base;  // hodograph slot: &smem[threadIdx.x]
   float4* far;   // parent ring:    &smem[4 * kThreads + threadIdx.x]
-  __device__ __forceinline__ void push(const Delta& f, uint32_t slot) const {
-    float4* q = far + slot * 4 * kThreads;
+  __device__ __forceinline__ void push(const Delta& f, float4 ival, uint32_t slot) const {
+    float4* q = far + slot * kRingF4 * kThreads;
     q[0] = f.p;
     q[kThreads] = f.d;
     q[2 * kThreads] = f.t0;
     q[3 * kThreads] = f.t1;
+    q[4 * kThreads] = ival;
   }
-  __device__ __forceinline__ void pop(Delta& f, uint32_t slot) const {
-    const float4* q = far + slot * 4 * kThreads;
+  __device__ __forceinline__ void pop(Delta& f, float4& ival, uint32_t slot) const {
+    const float4* q = far + slot * kRingF4 * kThreads;
     f.p = q[0];
     f.d = q[kThreads];
     f.t0 = q[2 * kThreads];
     f.t1 = q[3 * kThreads];
+    ival = q[4 * kThreads];
   }
   __device__ __forceinline__ void store(const Hodo& h) const {
     base[0] = h.L0;
@@ -531,8 +534,31 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
     }
   }
 #endif
-  if (!pass) return L.bits == 0u ? ST_MISS : ST_NEED_BT;  // done / backtrack
-  if (L.size <= min_size) {  // leaf: first hit terminates
+  // a5 for a cached far child is folded into the descent below: jump_up to the deepest
+  // pending level (the most recent push), then the far child of the cached parent is built
+  // with the same split arithmetic as the near child was, and its interval is the parent's
+  // with the split plane as its lower bound (a pending far child has c0 < t_P < c1, so the
+  // near child ended at t_P) -- its own slab (F7) in exact arithmetic.
+  bool bt = false, near_right = false;
+  if (!pass) {
+    if (L.bits == 0u) return ST_MISS;        // done
+    if (L.ncache == 0u) return ST_NEED_BT;   // re-calculation path (backtrack())
+    bt = true;
+    ++L.backtracks;
+    L.size = L.bits & (0u - L.bits);  // lowest pending bit (ctz), lst:bitstring P:1530-1542
+    L.start ^= L.size;
+    L.bits ^= L.size;
+    L.start &= ~(L.size - 1u);
+    float4 iv;
+    hs.pop(L.cur, iv, L.cache_top);  // the parent
+    near_right = (L.cache_right >> L.cache_top) & 1u;
+    L.cache_top = (L.cache_top + kFarCache - 1u) % kFarCache;
+    --L.ncache;
+    L.tmin = iv.x;
+    L.tmax = iv.y;
+    L.tag = __float_as_uint(iv.z);
+    L.terr = iv.w;
+  } else if (L.size <= min_size) {  // leaf: first hit terminates
     // the kind decision (F2, F6) matters only where the bound is a global cap or the ray
     // origin: LATERAL and WEDGE are one class with the same values (R3)
     const bool cap_bound = L.tag == TAG_ORIGIN || (L.tag == 0u && L.start == 0u) ||
@@ -547,32 +573,58 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
     L.c0 = c0;
     return ST_HIT;
   }
-  bool right, both;
-  float tP, kP;
-  const float tmin_in = L.tmin, tmax_in = L.tmax;
-  Split sp = partition(L.cur, c0, c1, L.tmin, L.tmax, L.tag, L.size > kCropMinSize,
-                       L.start + (L.size >> 1), right, both, tP, kP);
-  if (L.size > kCropMinSize) {
-    // near-ties of the near-child / both decisions and the error of the updated bound.
-    // Below the crop level these decisions only pick among nearly collinear leaves (the
-    // FP64 finalisation walks to the right one), so they are not re-run.
-    const float tauP = L.delta * (1.0f + kP);
-    L.tie |= ((fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP)) ? 16u : 0u;
-    if (L.tmin != tmin_in || L.tmax != tmax_in) L.terr = fmaxf(L.terr, tauP);
+  // the node being split (the current node, or the cached parent) and its plane
+  // (lst:subdivide_partition_and_update P:1429-1456)
+  const uint32_t psize = bt ? 2u * L.size : L.size;
+  const bool crop = psize > kCropMinSize;
+  Split sp;
+  split_geometry(L.cur, sp);
+  const float num = dot3(sp.tcn, sp.S), nz = sp.tcn.z;
+  const float rz = frcp(nz);
+  const float tP = num * rz;
+  const float kP = fminf((fabsf(sp.tcn.x) + fabsf(sp.tcn.y) + fabsf(nz)) * fabsf(rz), 1e30f);
+  const bool par = (nz == 0.0f);
+  const float tauP = L.delta * (1.0f + kP);
+  bool right;
+  if (!bt) {
+    right = par ? (num < 0.0f) : ((tP > c0) != (nz > 0.0f));  // near child (F9)
+    const bool both = !par && (c0 < tP) && (tP < c1);
+    const float4 ival = make_float4(L.tmin, L.tmax, __uint_as_float(L.tag), L.terr);
+    // one-bound update down to the crop level
+    const bool apply = crop && !par, up = tP > c0;
+    const bool hi_up = apply && up && tP < L.tmax;
+    const bool lo_up = apply && !up && tP > L.tmin;
+    L.tmax = hi_up ? tP : L.tmax;
+    L.tmin = lo_up ? tP : L.tmin;
+    L.tag = lo_up ? L.start + (L.size >> 1) : L.tag;
+    if (crop) {
+      // near-ties of the near-child / both decisions and the error of the updated bound.
+      // Below the crop level these decisions only pick among nearly collinear leaves, so
+      // they are not re-run.
+      L.tie |= ((fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP)) ? 16u : 0u;
+      if (hi_up | lo_up) L.terr = fmaxf(L.terr, tauP);
+    }
+    // go_down (lst:bitstring_manipulation P:1516-1528)
+    L.size >>= 1;
+    if (both) {
+      // remember the parent and its interval: the next jump_up returns to the deepest
+      // pending level, i.e. the most recent push (LIFO); the ring drops the oldest entry
+      L.bits |= L.size;
+      L.cache_top = (L.cache_top + 1u) % kFarCache;
+      hs.push(L.cur, ival, L.cache_top);
+      L.cache_right = right ? (L.cache_right | (1u << L.cache_top))
+                               : (L.cache_right & ~(1u << L.cache_top));
+      L.ncache = min(L.ncache + 1u, (uint32_t)kFarCache);
+    }
+    if (right) L.start |= L.size;
+  } else {
+    right = !near_right;
+    // the far child starts at the split plane (its tag: the split's u)
+    const bool lo_up = crop && tP > L.tmin;
+    L.tmin = lo_up ? tP : L.tmin;
+    L.tag = lo_up ? (right ? L.start : L.start + L.size) : L.tag;
+    if (lo_up) L.terr = fmaxf(L.terr, tauP);
   }
-  // go_down (lst:bitstring_manipulation P:1516-1528)
-  L.size >>= 1;
-  if (both) {
-    // remember the parent: the next jump_up returns to the deepest pending level, i.e.
-    // the most recent push (LIFO); the ring drops the oldest entry when full
-    L.bits |= L.size;
-    L.cache_top = (L.cache_top + 1u) % kFarCache;
-    hs.push(L.cur, L.cache_top);
-    L.cache_right = right ? (L.cache_right | (1u << L.cache_top))
-                             : (L.cache_right & ~(1u << L.cache_top));
-    L.ncache = min(L.ncache + 1u, (uint32_t)kFarCache);
-  }
-  if (right) L.start |= L.size;
   child(L.cur, sp, right, L.cur);
   if (L.size == kCropMinSize) {
     L.stmin = L.tmin;
@@ -583,25 +635,16 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
   return ST_RUNNING;
 }
 
-// jump_up to the deepest pending level, the far node's curve (rebuilt from
-// the cached parent, else re-calculated) and its own interval (F7).
+// jump_up to the deepest pending level when its parent is not in the ring:
+// the far node's curve re-calculated and its own interval (F7).
 __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
   ++L.backtracks;
   L.size = L.bits & (0u - L.bits);  // lowest pending bit (ctz)
   L.start ^= L.size;
   L.bits ^= L.size;
   L.start &= ~(L.size - 1u);
-  const bool cached = L.ncache > 0u;
-  if (cached) {
-    Delta parent;
-    hs.pop(parent, L.cache_top);
-    const bool near_right = (L.cache_right >> L.cache_top) & 1u;
-    Split sp;
-    split_geometry(parent, sp);
-    child(parent, sp, !near_right, L.cur);
-    L.cache_top = (L.cache_top + kFarCache - 1u) % kFarCache;
-    --L.ncache;
-  } else {
+  constexpr bool cached = false;  // cached far children are built inside step()
+  {
     float u0, u1;
     get_interval(L.start, L.size, u0, u1);
     recompute(hs.load(), u0, u1, L.cur);  // lst:recalculation P:1371-1385
