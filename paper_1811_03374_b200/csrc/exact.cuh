@@ -139,7 +139,9 @@ struct Result {
 // The whole traversal of one pair in FP64.
 __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1, const float4 P0,
                                         const float4 P1, const float4 P2, const float4 P3,
-                                        bool quad, int depth) {
+                                        bool quad, int depth, uint32_t start0 = 0u,
+                                        uint32_t size0 = 1u << FIBER_MAX_DEPTH,
+                                        uint32_t bits0 = 0u) {
   Result res{false, 0, 0, 0, 0, kOrigin, 0, 0, 0.0};
   // frame: o' = o + ts w^ next to the segment, ONB (Duff et al.)
   double wx = ray1.x, wy = ray1.y, wz = ray1.z;
@@ -169,13 +171,19 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
                          : Hodo64{L0, sub(L1, L0), sub(L2, L1), sub(L3, L2)};
   // ray interval [0, tmax) in local distance units
   const double lo0 = -ts, hi0 = (double)ray0.w * lw - ts;
-  Curve cur{L0, sub(L3, L0), hc.D0, hc.D2};
+  // resume at node (start0, size0) with the pending levels bits0 (the root by default): the
+  // node's curve re-calculated and its interval from its own end planes, as after a
+  // backtrack -- the carried interval of a descent equals it in exact
+  // arithmetic
+  const double inv23 = 1.0 / (double)(1u << FIBER_MAX_DEPTH);
+  Curve cur = size0 == (1u << FIBER_MAX_DEPTH)
+                  ? Curve{L0, sub(L3, L0), hc.D0, hc.D2}
+                  : node(hc, (double)start0 * inv23, (double)(start0 + size0) * inv23);
   double tmin, tmax;
   uint32_t tag;
-  slab(cur, lo0, hi0, 0u, 1u << FIBER_MAX_DEPTH, tmin, tmax, tag);
+  slab(cur, lo0, hi0, start0, start0 + size0, tmin, tmax, tag);
   const uint32_t min_size = 1u << (FIBER_MAX_DEPTH - depth);
-  uint32_t bits = 0, size = 1u << FIBER_MAX_DEPTH, start = 0, tests = 0, bt = 0;
-  const double inv23 = 1.0 / (double)(1u << FIBER_MAX_DEPTH);
+  uint32_t bits = bits0, size = size0, start = start0, tests = 0, bt = 0;
   while (true) {
     ++tests;
     double c0, c1;

@@ -22,7 +22,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kFarCache = 2;  // per-lane cache of pending far children
 constexpr int kRingF4 = 5;  // a ring entry: the parent's Delta (4 float4) + its interval
-constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache) * kThreads * sizeof(float4);
+constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache) * kThreads * sizeof(float4) +
+                               kThreads * sizeof(uint32_t);  // + the lanes' FP64 resume points
 
 // ------------------------------------------------------------------------------------
 // a7: FP64 finalisation (lst:calc_intersection P:1546-1587 with F2, F6, F8)
@@ -388,7 +389,8 @@ struct Lane {
   float stmin, stmax;  // interval saved at level kCropLevel (deep backtracks)
   float delta;         // FP32 error scale of the local coordinates: 2^-20 max|coordinate|
   float terr, sterr;   // error bound of the current (saved) interval bounds
-  uint32_t tie;        // near-tie decisions seen (bit mask): re-run the pair in FP64 (in K3)
+  uint32_t tie;        // 0, or after the first near-tie decision: the resume point's pending
+                       // bits | the tie kinds seen (bits 0-4): re-run the pair in FP64 (K3)
   uint32_t tag, stag, bits, start, size, tests, backtracks;
   uint32_t ncache, cache_top, cache_right;  // parent-cache fill, ring top, near-side bits
 };
@@ -401,6 +403,7 @@ enum : int { ST_RUNNING = 0, ST_MISS = 1, ST_HIT = 2, ST_NEED_BT = 3 };
 struct HodoRef {
   float4* base;  // hodograph slot: &smem[threadIdx.x]
   float4* far;   // parent ring:    &smem[4 * kThreads + threadIdx.x]
+  uint32_t* rs;  // FP64 resume point (start | log2(size) << 24), written at the first tie
   __device__ __forceinline__ void push(const Delta& f, float4 ival, uint32_t slot) const {
     float4* q = far + slot * kRingF4 * kThreads;
     q[0] = f.p;
@@ -507,6 +510,24 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   return true;
 }
 
+// Record near-tie kinds t of the current node's decisions.  At the first one, the FP64
+// re-run's resume point is fixed: every earlier decision was certain, so the FP64 traversal
+// may start at this node (its curve and interval re-derived exactly) with the pending
+// levels above it.  Below the crop level the FP32 path is uncropped and may have strayed
+// from the oracle's, so the resume point is the node's crop-level ancestor (the pending bits
+// of deeper levels dropped).  Pending far children above the resume node are at least
+// kCropMinSize, so bits 0-4 are free for the kinds.
+__device__ __forceinline__ void note_tie(Lane& L, HodoRef hs, uint32_t t) {
+  if (t != 0u && L.tie == 0u) {
+    const bool deep = L.size < kCropMinSize;
+    const uint32_t st = deep ? (L.start & ~(kCropMinSize - 1u)) : L.start;
+    const uint32_t sz = deep ? kCropMinSize : L.size;
+    *hs.rs = st | ((31u - __clz(sz)) << 24);
+    L.tie = deep ? (L.bits & ~(kCropMinSize - 1u)) : L.bits;
+  }
+  L.tie |= t;
+}
+
 // One iteration: node test, then descend.  Returns ST_RUNNING, ST_MISS, ST_HIT (leaf
 // accepted; L.c0 holds the cylinder entry) or ST_NEED_BT (pruned with levels pending).
 __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
@@ -520,9 +541,9 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
   // delta / sin(ray, axis), the interval bounds L.terr
   const float tau = L.delta * fmaf(2.0f, inv_sin, 2.0f);
   const float tb = tau + L.terr;
-  L.tie |= (tie_e < 0.0f ? 1u : 0u) |
-           ((cyl && ((fabsf(c1 - L.tmin) < tb) | (fabsf(L.tmax - c0) < tb) |
-                     (fabsf(L.tmax - L.tmin) < 2.0f * L.terr))) ? 2u : 0u);
+  note_tie(L, hs, (tie_e < 0.0f ? 1u : 0u) |
+                  ((cyl && ((fabsf(c1 - L.tmin) < tb) | (fabsf(L.tmax - c0) < tb) |
+                            (fabsf(L.tmax - L.tmin) < 2.0f * L.terr))) ? 2u : 0u));
 #ifdef FIBER_TRACE
   if (trace) {
     unsigned k = atomicAdd(&g_trace_n, 1u);
@@ -564,12 +585,12 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
     const bool cap_bound = L.tag == TAG_ORIGIN || (L.tag == 0u && L.start == 0u) ||
                            (L.tag == (1u << FIBER_MAX_DEPTH) &&
                             L.start + L.size == (1u << FIBER_MAX_DEPTH));
-    L.tie |= (cap_bound && fabsf(c0 - L.tmin) < tb) ? 4u : 0u;
+    note_tie(L, hs, (cap_bound && fabsf(c0 - L.tmin) < tb) ? 4u : 0u);
     // below the crop level the leaf index is only known to about (error of c0 along the
     // axis) / (leaf length) = tau |d_z| / |d|^2 leaves; K3 walks up to kWalk of them, so
     // nearly parallel rays that could be further off are re-run in FP64
     if (L.size < kCropMinSize)
-      L.tie |= L.delta * inv_sin * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d) ? 8u : 0u;
+      note_tie(L, hs, L.delta * inv_sin * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d) ? 8u : 0u);
     L.c0 = c0;
     return ST_HIT;
   }
@@ -601,7 +622,7 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
       // near-ties of the near-child / both decisions and the error of the updated bound.
       // Below the crop level these decisions only pick among nearly collinear leaves, so
       // they are not re-run.
-      L.tie |= ((fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP)) ? 16u : 0u;
+      note_tie(L, hs, ((fabsf(tP - c0) < tau + tauP) | (fabsf(tP - c1) < tau + tauP)) ? 16u : 0u);
       if (hi_up | lo_up) L.terr = fmaxf(L.terr, tauP);
     }
     // go_down (lst:bitstring_manipulation P:1516-1528)
@@ -680,7 +701,8 @@ __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
 __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane& L, int st,
                                          uint32_t badseg, HodoRef hs) {
   if (L.tie) {  // decided by a near-tie somewhere: K3 re-runs the pair in FP64
-    p.hits[i] = make_float4(0.0f, __uint_as_float(L.tie), 0.0f, __uint_as_float(badseg | kUncertain));
+    p.hits[i] = make_float4(__uint_as_float(*hs.rs), __uint_as_float(L.tie & 31u),
+                            __uint_as_float(L.tie & ~31u), __uint_as_float(badseg | kUncertain));
     p.list_exact[atomicAdd(&p.counter[4], 1u)] = i;
     return;
   }
@@ -798,8 +820,14 @@ __device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
 // pair alone (independent of the launch shape and of the schedule).  Hits leave
 // provisional records that K3 finalises.
 // ------------------------------------------------------------------------------------
-constexpr int kEpoch = 2;
-constexpr uint32_t kRefill = 16;
+#ifndef FIBER_EPOCH
+#define FIBER_EPOCH 2
+#endif
+#ifndef FIBER_REFILL
+#define FIBER_REFILL 16
+#endif
+constexpr int kEpoch = FIBER_EPOCH;          // iterations between refill votes
+constexpr uint32_t kRefill = FIBER_REFILL;  // idle lanes that trigger a refill
 
 __device__ __forceinline__ void start_lane(const Prepared& e, Lane& L, HodoRef hs) {
   hs.store(e.h);
@@ -833,7 +861,8 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
   extern __shared__ float4 smem[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
-  HodoRef hs{&smem[threadIdx.x], &smem[4 * kThreads + threadIdx.x]};
+  HodoRef hs{&smem[threadIdx.x], &smem[4 * kThreads + threadIdx.x],
+             reinterpret_cast<uint32_t*>(&smem[(4 + kRingF4 * kFarCache) * kThreads]) + threadIdx.x};
   const uint32_t min_size = p.min_size;
   Lane L;
   uint32_t pair = 0, badseg = 0;
@@ -915,7 +944,12 @@ __device__ __noinline__ void exact_one(const Params& p, uint32_t i) {
   const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
   const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
   const bool quad = (__ldg(&p.sflags[pr.y]) & FIBER_SEG_QUADRATIC) != 0u;
-  const exact::Result r = exact::traverse(ray0, ray1, P0, P1, P2, P3, quad, p.depth);
+  // resume where K2 saw its first near-tie (note_tie): start | log2(size) << 24, bits
+  const float4 rec = p.hits[i];
+  const uint32_t rs = __float_as_uint(rec.x), rbits = __float_as_uint(rec.z);
+  const uint32_t rstart = rs & 0x00ffffffu, rsize = 1u << (rs >> 24);
+  const exact::Result r = exact::traverse(ray0, ray1, P0, P1, P2, P3, quad, p.depth, rstart,
+                                          rsize, rbits);
   const uint32_t cnt = (min(r.backtracks, 255u) << 8) | (min(r.tests, 65535u) << 16);
   if (r.hit) {
     p.hits[i] = make_float4(0.0f, __uint_as_float(r.start | (r.kind << 24) | (r.inside << 26) | kExactLeaf),
