@@ -230,12 +230,16 @@ def run_ours(args):
         "hit_fraction_by_depth": {str(D): round(float(np.mean(
             [hitfrac[j] for j, (fi, d) in enumerate(launches) if d == D])), 4) for D in DEPTHS},
         "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                     "traffic": _k2_traffic(),
+                     "algorithmic_bytes_per_launch": 56 * n,
                      "peak_basis": f"FP32: {sms} SMs x 128 lanes x 2 x {peak_mhz:.0f} MHz "
                                    "(max SM clock; B200_PROFILING.md unit counts)",
                      "kernel": "intersect_kernel (K2), timed alone with CUDA events",
                      "k2_share_of_step": round(float(k2_ms.sum() / mean_ms.sum()), 3),
-                     "traffic_note": "see profiles/ (ncu dram bytes per K2 launch)"},
+                     "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one K2 "
+                                     "launch (fiber A, D=22, 2^20 pairs) from the committed ncu "
+                                     "--set full summary " + TRAFFIC_PROFILE},
         "gpu_launches": args.steps * len(launches) * 2,
         "clocks": clocks,
         "wall_s_timed": round(wall, 3),
@@ -327,6 +331,26 @@ def _time_oracle(ws, nthreads):
                              nthreads=nthreads)
             n += w.n_pairs
     return n, time.perf_counter() - t0
+
+
+TRAFFIC_PROFILE = "profiles/r1_full_K2K3_fiberA_D22.txt"
+
+
+def _k2_traffic():
+    """DRAM bytes (read + write) of one K2 launch from the committed ncu summary, or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), TRAFFIC_PROFILE)
+    if not os.path.exists(path):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total, in_k2 = 0.0, False
+    for line in open(path):
+        if line.startswith("## "):
+            in_k2 = line.startswith("## intersect_kernel")
+        elif in_k2 and line.split()[:1] and line.split()[0] in ("dram__bytes_read.sum",
+                                                                 "dram__bytes_write.sum"):
+            parts = line.split()
+            total += float(parts[1]) * scale.get(parts[2], 1)
+    return int(total) if total else None
 
 
 def cpu_baseline(n_per: int = 1 << 17):
