@@ -22,95 +22,88 @@
 
 namespace fibergk {
 
-constexpr int kMaxDeg = 8;
-
-struct BP {  // polynomial in the Bernstein basis of degree n on [0, 1]
-  int n;
-  double b[kMaxDeg + 1];
+// Polynomials in the Bernstein basis of fixed degree N on [0, 1] (degrees are template
+// parameters, so the coefficient arrays live in registers and the loops unroll).
+template <int N>
+struct BP {
+  double b[N + 1];
 };
 
-__device__ __forceinline__ double binom(int n, int k) {
-  // n <= 8
-  const double row[9][9] = {
-      {1}, {1, 1}, {1, 2, 1}, {1, 3, 3, 1}, {1, 4, 6, 4, 1}, {1, 5, 10, 10, 5, 1},
-      {1, 6, 15, 20, 15, 6, 1}, {1, 7, 21, 35, 35, 21, 7, 1}, {1, 8, 28, 56, 70, 56, 28, 8, 1}};
-  return row[n][k];
-}
-
-__device__ inline BP bp_mul(const BP& f, const BP& g) {
-  BP r;
-  r.n = f.n + g.n;
-  for (int k = 0; k <= r.n; ++k) r.b[k] = 0.0;
-  for (int i = 0; i <= f.n; ++i)
-    for (int j = 0; j <= g.n; ++j) r.b[i + j] += binom(f.n, i) * binom(g.n, j) * f.b[i] * g.b[j];
-  for (int k = 0; k <= r.n; ++k) r.b[k] /= binom(r.n, k);
+__host__ __device__ constexpr double binom(int n, int k) {
+  double r = 1.0;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
   return r;
 }
 
-__device__ inline BP bp_elevate(const BP& f, int N) {
-  BP r;
-  r.n = N;
-  for (int k = 0; k <= N; ++k) {
+template <int M, int N>
+__device__ __forceinline__ BP<M + N> bp_mul(const BP<M>& f, const BP<N>& g) {
+  BP<M + N> r;
+#pragma unroll
+  for (int k = 0; k <= M + N; ++k) r.b[k] = 0.0;
+#pragma unroll
+  for (int i = 0; i <= M; ++i)
+#pragma unroll
+    for (int j = 0; j <= N; ++j) r.b[i + j] += (binom(M, i) * binom(N, j)) * f.b[i] * g.b[j];
+#pragma unroll
+  for (int k = 0; k <= M + N; ++k) r.b[k] *= 1.0 / binom(M + N, k);
+  return r;
+}
+
+template <int N, int M>
+__device__ __forceinline__ BP<M> bp_elevate(const BP<N>& f) {
+  BP<M> r;
+#pragma unroll
+  for (int k = 0; k <= M; ++k) {
     double acc = 0.0;
-    for (int i = 0; i <= f.n; ++i)
-      if (k - i >= 0 && k - i <= N - f.n) acc += binom(f.n, i) * binom(N - f.n, k - i) * f.b[i];
-    r.b[k] = acc / binom(N, k);
+#pragma unroll
+    for (int i = 0; i <= N; ++i)
+      if (k - i >= 0 && k - i <= M - N) acc += (binom(N, i) * binom(M - N, k - i)) * f.b[i];
+    r.b[k] = acc * (1.0 / binom(M, k));
   }
-  return r;
-}
-
-__device__ inline BP bp_axpy(double a, const BP& f, const BP& g) {  // a f + g
-  const int N = f.n > g.n ? f.n : g.n;
-  const BP F = bp_elevate(f, N), G = bp_elevate(g, N);
-  BP r;
-  r.n = N;
-  for (int k = 0; k <= N; ++k) r.b[k] = a * F.b[k] + G.b[k];
   return r;
 }
 
 // True iff f(u) < -tol for some u in [0, 1], certified by the convex hull of the Bernstein
 // coefficients and de Casteljau halving (depth-first, explicit stack).  At the depth limit
 // the midpoint value decides (the polynomial is then within rounding of a root).
-__device__ inline bool bp_negative_somewhere(const BP& f0, double tol) {
-  constexpr int kStack = 48, kMaxLevel = 40;
-  BP st[kStack];
-  int lv[kStack];
+template <int N>
+__device__ __noinline__ bool bp_negative_somewhere(const BP<N> f0, double tol) {
+  constexpr int kStack = 44, kMaxLevel = 40;
+  BP<N> st[kStack];
+  unsigned char lv[kStack];
   int top = 0;
   st[0] = f0;
   lv[0] = 0;
   while (top >= 0) {
-    const BP f = st[top];
+    const BP<N> f = st[top];
     const int level = lv[top];
     --top;
-    if (f.b[0] < -tol || f.b[f.n] < -tol) return true;  // an end value
+    if (f.b[0] < -tol || f.b[N] < -tol) return true;  // an end value
     double mn = f.b[0];
-    for (int k = 1; k <= f.n; ++k) mn = fmin(mn, f.b[k]);
+#pragma unroll
+    for (int k = 1; k <= N; ++k) mn = fmin(mn, f.b[k]);
     if (mn >= -tol) continue;  // hull above -tol on this interval
+    double w[N + 1];
+#pragma unroll
+    for (int k = 0; k <= N; ++k) w[k] = f.b[k];
+    BP<N> L, R;
+    L.b[0] = w[0];
+    R.b[N] = w[N];
+#pragma unroll
+    for (int r = 1; r <= N; ++r) {
+#pragma unroll
+      for (int k = 0; k <= N - r; ++k) w[k] = 0.5 * (w[k] + w[k + 1]);
+      L.b[r] = w[0];
+      R.b[N - r] = w[N - r];
+    }
     if (level >= kMaxLevel || top + 2 >= kStack) {
-      // value at the midpoint
-      double w[kMaxDeg + 1];
-      for (int k = 0; k <= f.n; ++k) w[k] = f.b[k];
-      for (int r = 1; r <= f.n; ++r)
-        for (int k = 0; k <= f.n - r; ++k) w[k] = 0.5 * (w[k] + w[k + 1]);
-      if (w[0] < -tol) return true;
+      if (R.b[0] < -tol) return true;  // the midpoint value
       continue;
     }
-    // de Casteljau at 1/2: left = first column, right = last diagonal
-    double w[kMaxDeg + 1];
-    BP L, R;
-    L.n = R.n = f.n;
-    for (int k = 0; k <= f.n; ++k) w[k] = f.b[k];
-    L.b[0] = w[0];
-    R.b[f.n] = w[f.n];
-    for (int r = 1; r <= f.n; ++r) {
-      for (int k = 0; k <= f.n - r; ++k) w[k] = 0.5 * (w[k] + w[k + 1]);
-      L.b[r] = w[0];
-      R.b[f.n - r] = w[f.n - r];
-    }
     st[++top] = R;
-    lv[top] = level + 1;
+    lv[top] = (unsigned char)(level + 1);
     st[++top] = L;  // left first
-    lv[top] = level + 1;
+    lv[top] = (unsigned char)(level + 1);
   }
   return false;
 }
@@ -120,76 +113,90 @@ __device__ inline bool bp_negative_somewhere(const BP& f0, double tol) {
 // largest radius control point (parametric = false) or the cubic radius (true).
 __device__ inline bool end_crossed(const double Pin[4][4], int end, bool parametric) {
   double P[4][4];
+#pragma unroll
   for (int i = 0; i < 4; ++i)
+#pragma unroll
     for (int k = 0; k < 4; ++k) P[i][k] = end ? Pin[i][k] : Pin[3 - i][k];
   // scale-free coordinates: relative to p0, divided by the chord length
   double ch = 0.0;
+#pragma unroll
   for (int k = 0; k < 3; ++k) ch += (P[3][k] - P[0][k]) * (P[3][k] - P[0][k]);
   ch = sqrt(ch);
   if (!(ch > 0.0)) return true;
   const double is = 1.0 / ch;
   double Q[4][3];
+#pragma unroll
   for (int i = 0; i < 4; ++i)
+#pragma unroll
     for (int k = 0; k < 3; ++k) Q[i][k] = (P[i][k] - P[0][k]) * is;
   double T[3][3], t1[3];
+#pragma unroll
   for (int j = 0; j < 3; ++j)
+#pragma unroll
     for (int k = 0; k < 3; ++k) T[j][k] = 3.0 * (Q[j + 1][k] - Q[j][k]);
+#pragma unroll
   for (int k = 0; k < 3; ++k) t1[k] = T[2][k];
   // A~ (degree 2): A_i = <Q3 - Q_i, t1>, A_3 = 0, divided by (1 - u): A~_i = A_i 3 / (3 - i)
-  BP At;
-  At.n = 2;
+  BP<2> At;
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
     double a = 0.0;
+#pragma unroll
     for (int k = 0; k < 3; ++k) a += (Q[3][k] - Q[i][k]) * t1[k];
     At.b[i] = a * 3.0 / (3.0 - i);
   }
-  // |T|^2 (degree 4) and X~ = (T x t1) / (1 - u) (degree 1): X_j 2 / (2 - j), X_2 = 0
-  BP T2;
-  T2.n = 4;
+  // |T|^2 (degree 4) and |X~|^2, X~ = (T x t1) / (1 - u) (degree 1): X_j 2 / (2 - j), X_2 = 0
+  BP<4> T2;
+  BP<2> X2;
+#pragma unroll
   for (int k = 0; k <= 4; ++k) T2.b[k] = 0.0;
-  BP X2;
-  X2.n = 2;
+#pragma unroll
   for (int k = 0; k <= 2; ++k) X2.b[k] = 0.0;
   double Xt[2][3];
+#pragma unroll
   for (int j = 0; j < 2; ++j) {
     const double* a = T[j];
     Xt[j][0] = (a[1] * t1[2] - a[2] * t1[1]) * 2.0 / (2.0 - j);
     Xt[j][1] = (a[2] * t1[0] - a[0] * t1[2]) * 2.0 / (2.0 - j);
     Xt[j][2] = (a[0] * t1[1] - a[1] * t1[0]) * 2.0 / (2.0 - j);
   }
+#pragma unroll
   for (int c = 0; c < 3; ++c) {
-    BP tc;
-    tc.n = 2;
+    BP<2> tc;
+#pragma unroll
     for (int j = 0; j < 3; ++j) tc.b[j] = T[j][c];
-    const BP sq = bp_mul(tc, tc);
+    const BP<4> sq = bp_mul(tc, tc);
+#pragma unroll
     for (int k = 0; k <= 4; ++k) T2.b[k] += sq.b[k];
-    BP xc;
-    xc.n = 1;
+    BP<1> xc;
     xc.b[0] = Xt[0][c];
     xc.b[1] = Xt[1][c];
-    const BP xs = bp_mul(xc, xc);
+    const BP<2> xs = bp_mul(xc, xc);
+#pragma unroll
     for (int k = 0; k <= 2; ++k) X2.b[k] += xs.b[k];
   }
-  BP R2;
+  BP<8> rhs;
   if (parametric) {
-    BP r;
-    r.n = 3;
+    BP<3> r;
+#pragma unroll
     for (int i = 0; i < 4; ++i) r.b[i] = P[i][3] * is;
-    R2 = bp_mul(r, r);
+    rhs = bp_mul(bp_mul(r, r), X2);
   } else {
     const double rb = fmax(fmax(P[0][3], P[1][3]), fmax(P[2][3], P[3][3])) * is;
-    R2.n = 0;
-    R2.b[0] = rb * rb;
+    const BP<8> x8 = bp_elevate<2, 8>(X2);
+#pragma unroll
+    for (int k = 0; k <= 8; ++k) rhs.b[k] = rb * rb * x8.b[k];
   }
-  const BP lhs = bp_mul(bp_mul(At, At), T2);  // degree 8
-  const BP rhs = bp_mul(R2, X2);               // degree 8 or 2
-  const BP F = bp_axpy(-1.0, rhs, lhs);
+  const BP<8> lhs = bp_mul(bp_mul(At, At), T2);
+  BP<8> F;
   double sc = 0.0;
-  for (int k = 0; k <= lhs.n; ++k) sc = fmax(sc, fabs(lhs.b[k]));
-  for (int k = 0; k <= rhs.n; ++k) sc = fmax(sc, fabs(rhs.b[k]));
-  double sa = 0.0;
-  for (int k = 0; k <= 2; ++k) sa = fmax(sa, fabs(At.b[k]));
-  return bp_negative_somewhere(At, 1e-13 * sa) || bp_negative_somewhere(F, 1e-13 * sc);
+#pragma unroll
+  for (int k = 0; k <= 8; ++k) {
+    F.b[k] = lhs.b[k] - rhs.b[k];
+    sc = fmax(sc, fmax(fabs(lhs.b[k]), fabs(rhs.b[k])));
+  }
+  const double sa = fmax(fabs(At.b[0]), fmax(fabs(At.b[1]), fabs(At.b[2])));
+  return bp_negative_somewhere<2>(At, 1e-13 * sa) || bp_negative_somewhere<8>(F, 1e-13 * sc);
 }
 
 // The five cubic constraints hold (>= 0) on the positions of P.

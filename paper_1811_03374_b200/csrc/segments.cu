@@ -20,8 +20,12 @@ __device__ uint32_t thick_flags(const double P[4][3], const float r[4]) {
     Q[i][3] = r[i];
   }
   uint32_t f = 0;
-  if (fibergk::end_crossed(Q, 0, false) || fibergk::end_crossed(Q, 1, false)) f |= FIBER_SEG_THICK;
-  if (fibergk::end_crossed(Q, 0, true) || fibergk::end_crossed(Q, 1, true)) f |= FIBER_SEG_THICK_PARAM;
+  if (fibergk::end_crossed(Q, 0, false) || fibergk::end_crossed(Q, 1, false)) {
+    f |= FIBER_SEG_THICK;
+    // r(u) <= r_bar: the exact surface can only cross where the r_bar surface does
+    if (fibergk::end_crossed(Q, 0, true) || fibergk::end_crossed(Q, 1, true))
+      f |= FIBER_SEG_THICK_PARAM;
+  }
   return f;
 }
 
