@@ -232,14 +232,20 @@ def run_ours(args):
         "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                      "traffic": _k2_traffic(),
+                     "issue_active_pct": _k2_profile_metrics().get(
+                         "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                     "simt_lanes": _k2_profile_metrics().get(
+                         "smsp__thread_inst_executed_per_inst_executed.ratio"),
                      "algorithmic_bytes_per_launch": 56 * n,
                      "peak_basis": f"FP32: {sms} SMs x 128 lanes x 2 x {peak_mhz:.0f} MHz "
                                    "(max SM clock; B200_PROFILING.md unit counts)",
                      "kernel": "intersect_kernel (K2), timed alone with CUDA events",
                      "k2_share_of_step": round(float(k2_ms.sum() / mean_ms.sum()), 3),
-                     "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one K2 "
-                                     "launch (fiber A, D=22, 2^20 pairs) from the committed ncu "
-                                     "--set full summary " + TRAFFIC_PROFILE},
+                     "traffic_note": "traffic, issue_active_pct and simt_lanes: one K2 launch "
+                                     "(fiber A, D=22, 2^20 pairs) in the committed ncu --set full "
+                                     "summary " + TRAFFIC_PROFILE + "; the kernel is bound by "
+                                     "instruction issue (comparisons, selects, MUFU), not by "
+                                     "FP32 flops"},
         "gpu_launches": args.steps * len(launches) * 2,
         "clocks": clocks,
         "wall_s_timed": round(wall, 3),
@@ -361,21 +367,30 @@ def _time_oracle(ws, nthreads):
 TRAFFIC_PROFILE = "profiles/r1_full_K2K3_fiberA_D22.txt"
 
 
-def _k2_traffic():
-    """DRAM bytes (read + write) of one K2 launch from the committed ncu summary, or None."""
+def _k2_profile_metrics() -> dict:
+    """K2's metrics in the committed ncu --set full summary (TRAFFIC_PROFILE), by name."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), TRAFFIC_PROFILE)
+    out, in_k2 = {}, False
     if not os.path.exists(path):
-        return None
+        return out
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    total, in_k2 = 0.0, False
     for line in open(path):
         if line.startswith("## "):
             in_k2 = line.startswith("## intersect_kernel")
-        elif in_k2 and line.split()[:1] and line.split()[0] in ("dram__bytes_read.sum",
-                                                                 "dram__bytes_write.sum"):
+        elif in_k2 and len(line.split()) >= 2:
             parts = line.split()
-            total += float(parts[1]) * scale.get(parts[2], 1)
-    return int(total) if total else None
+            try:
+                out[parts[0]] = float(parts[1]) * (scale.get(parts[2], 1) if len(parts) > 2 else 1)
+            except ValueError:
+                pass
+    return out
+
+
+def _k2_traffic():
+    """DRAM bytes (read + write) of one K2 launch from the committed ncu summary, or None."""
+    m = _k2_profile_metrics()
+    t = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+    return int(t) if t else None
 
 
 def cpu_baseline(n_per: int = 1 << 17):
