@@ -79,6 +79,31 @@ def test_glancing_rays_parity(fx, depth, radius):
     assert rep["hits"] > 0.5 * (1 << 14)
 
 
+@pytest.mark.parametrize("shape", ["quarter_z", "fiberC"])
+@pytest.mark.parametrize("radius", [0.1, 0.3])
+@pytest.mark.parametrize("depth", [1, 2, 3, 4, 6])
+def test_curved_thick_low_depth_parity(fx, shape, radius, depth):
+    """Strongly curved, thick fibers at low depth (R9): the far child of a cached
+    backtrack takes the parent's interval cut at the split plane, and K3 resumes at a node with
+    its own slab; on valid fibers the older crop planes never cut a node's cylinder, so both
+    equal the oracle's intervals where they matter."""
+    k = 4 / 3 * (np.sqrt(2) - 1)
+    c = {"quarter_z": np.array([[1, 0, 0], [1, k, 0.2], [k, 1, -0.2], [0, 1, 0]]),
+         "fiberC": gen.FIBER_C}[shape]
+    ctrl = c[None].astype(np.float32)
+    radii = np.full((1, 4), radius, np.float32)
+    rng = np.random.default_rng(5)
+    n = 1 << 14
+    lo, hi = c.min(0) - radius, c.max(0) + radius
+    tgt = lo + (hi - lo) * rng.uniform(0, 1, (n, 3))
+    orig = 0.5 * (lo + hi) + 3 * gen._sphere(rng, n)
+    w = gen.Workload("curved", gen._pack_rays(orig, tgt - orig), ctrl, radii,
+                     gen.make_pairs_1seg(n), depth)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+    assert rep["hits"] > 2000
+
+
 def test_spec_example_all_depths(fx):
     ctrl, radii = gen.straight_fiber()
     rays = np.array([[3, 0, -5, np.inf, 0, 0, 1, 0]], np.float32)
