@@ -210,6 +210,21 @@ int fiber_grid_candidates(const fiber_grid *grid, const fiber_ray *rays, int64_t
                           const uint32_t *offsets, uint32_t max_count, int order,
                           fiber_pair *pairs, void *cuda_stream);
 
+/* Closest hit over the grid's candidates with early termination (SURVEY 8(f) rows 2 + 3):
+ * rounds of (walk: each active ray's DDA emits its next k candidates, k = 8, 16, ... 256;
+ * fiber_intersect_closest on them) until every ray's walk is over or its best hit lies
+ * strictly before the walk's position -- exact, since a later candidate enters its box at or
+ * after that position and its hits lie in the box.
+ *   nearest  device uint64[n_rays], initialised by the caller (fiber_nearest_init); on return
+ *            nearest[r] = min over r's candidates of (bits(t) << 32) | segment index -- keys
+ *            carry the SEGMENT (not a pair index), so the result does not depend on the order
+ *            of the rounds.
+ *   rounds   (host, may be NULL) the number of rounds run.
+ * Synchronises the stream once per round.  Errors: FIBER_EINVAL, FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_grid_closest(const fiber_grid *grid, const fiber_ray *rays, int64_t n_rays,
+                       const fiber_segments *segs, int max_depth, uint64_t *nearest,
+                       int *rounds, void *cuda_stream);
+
 /* The hot path (lst:algorithm): for every pair, intersect rays[pair.ray] with
  * segment pair.seg at subdivision depth max_depth and write hits[i].
  *   rays      device fiber_ray[n_rays]

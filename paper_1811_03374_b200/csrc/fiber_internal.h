@@ -10,3 +10,8 @@ int set_error(int code, const char* msg);
 int check_device();
 // Turn cudaGetLastError() after a launch into FIBER_OK / FIBER_ECUDA.
 int check_launch(const char* what);
+// K2 + K3 on device pairs with nearest keys only (intersect.cu): mode bit 0 = the running
+// t_max bound of fiber_intersect_closest, bit 1 = keys carry the segment index.
+int launch_intersect_mode(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
+                          const fiber_pair* pairs, int64_t n_pairs, int max_depth,
+                          uint64_t* nearest, void* stream, int mode);

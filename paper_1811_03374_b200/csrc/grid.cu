@@ -183,63 +183,113 @@ __device__ __forceinline__ bool box_entry(const float o[3], const float id[3], f
   return a <= b;
 }
 
-// The DDA: calls emit(seg) for every candidate of the ray in front-to-back cell order.
-template <class Emit>
-__device__ void walk(const GridView& g, float4 r0, float4 r1, Emit emit) {
-  const float o[3] = {r0.x, r0.y, r0.z}, d[3] = {r1.x, r1.y, r1.z};
-  float id[3];
-  for (int k = 0; k < 3; ++k) id[k] = 1.0f / d[k];  // +-inf for a zero component
+// The DDA, resumable: per-ray constants and an 8-word state (the current cell, the axis
+// crossings, the cell's entry t and a cursor into its segment list).  walk() emits every
+// candidate of the ray in front-to-back cell order; dda_walk() emits up to kmax and can be
+// resumed where it stopped, emitting the same sequence.
+struct RayDDA {
+  float o[3], d[3], id[3];
+  float t0, t1;
+  int step[3];
+  float tdelta[3];
+};
+struct DDAState {
+  int c[3];  // c[0] < 0: the walk is over
+  float tnext[3];
+  float tin;
+  uint32_t cursor;
+};
+
+__device__ bool dda_setup(const GridView& g, float4 r0, float4 r1, RayDDA& R, DDAState& S) {
+  R.o[0] = r0.x, R.o[1] = r0.y, R.o[2] = r0.z;
+  R.d[0] = r1.x, R.d[1] = r1.y, R.d[2] = r1.z;
+  for (int k = 0; k < 3; ++k) R.id[k] = 1.0f / R.d[k];  // +-inf for a zero component
   // clip [0, tmax) to the grid box
   float t0 = 0.0f, t1 = r0.w;
   for (int k = 0; k < 3; ++k) {
     const float lo = g.lo[k], hi = g.lo[k] + g.dims[k] * g.cell[k];
-    if (d[k] == 0.0f) {
-      if (o[k] < lo || o[k] > hi) return;
+    if (R.d[k] == 0.0f) {
+      if (R.o[k] < lo || R.o[k] > hi) t1 = -1.0f;
       continue;
     }
-    float x = (lo - o[k]) * id[k], y = (hi - o[k]) * id[k];
+    float x = (lo - R.o[k]) * R.id[k], y = (hi - R.o[k]) * R.id[k];
     t0 = fmaxf(t0, fminf(x, y));
     t1 = fminf(t1, fmaxf(x, y));
   }
-  if (!(t0 <= t1)) return;
-  int c[3], step[3];
-  float tnext[3], tdelta[3];
+  R.t0 = t0;
+  R.t1 = t1;
   for (int k = 0; k < 3; ++k) {
-    const float p = o[k] + t0 * d[k];
-    c[k] = max(0, min(g.dims[k] - 1, (int)floorf((p - g.lo[k]) * g.inv_cell[k])));
-    if (d[k] > 0.0f) {
-      step[k] = 1;
-      tnext[k] = (g.lo[k] + (c[k] + 1) * g.cell[k] - o[k]) * id[k];
-      tdelta[k] = g.cell[k] * id[k];
-    } else if (d[k] < 0.0f) {
-      step[k] = -1;
-      tnext[k] = (g.lo[k] + c[k] * g.cell[k] - o[k]) * id[k];
-      tdelta[k] = -g.cell[k] * id[k];
+    const float p = R.o[k] + t0 * R.d[k];
+    S.c[k] = max(0, min(g.dims[k] - 1, (int)floorf((p - g.lo[k]) * g.inv_cell[k])));
+    if (R.d[k] > 0.0f) {
+      R.step[k] = 1;
+      S.tnext[k] = (g.lo[k] + (S.c[k] + 1) * g.cell[k] - R.o[k]) * R.id[k];
+      R.tdelta[k] = g.cell[k] * R.id[k];
+    } else if (R.d[k] < 0.0f) {
+      R.step[k] = -1;
+      S.tnext[k] = (g.lo[k] + S.c[k] * g.cell[k] - R.o[k]) * R.id[k];
+      R.tdelta[k] = -g.cell[k] * R.id[k];
     } else {
-      step[k] = 0;
-      tnext[k] = INFINITY;
-      tdelta[k] = INFINITY;
+      R.step[k] = 0;
+      S.tnext[k] = INFINITY;
+      R.tdelta[k] = INFINITY;
     }
   }
-  float tin = t0;
-  while (true) {
-    const int ax = tnext[0] <= tnext[1] ? (tnext[0] <= tnext[2] ? 0 : 2) : (tnext[1] <= tnext[2] ? 1 : 2);
+  S.tin = t0;
+  S.cursor = 0;
+  if (!(t0 <= t1)) S.c[0] = -1;
+  return S.c[0] >= 0;
+}
+
+// Re-derive the constants of a ray whose state is stored (the setup is deterministic).
+__device__ void dda_consts(const GridView& g, float4 r0, float4 r1, RayDDA& R) {
+  DDAState tmp;
+  dda_setup(g, r0, r1, R, tmp);
+}
+
+template <class Emit>
+__device__ uint32_t dda_walk(const GridView& g, const RayDDA& R, DDAState& S, uint32_t kmax,
+                             Emit emit) {
+  uint32_t n = 0;
+  while (S.c[0] >= 0) {
+    const int ax = S.tnext[0] <= S.tnext[1] ? (S.tnext[0] <= S.tnext[2] ? 0 : 2)
+                                            : (S.tnext[1] <= S.tnext[2] ? 1 : 2);
     // the last cell (the ray ends in it, or the next step leaves the grid) extends to t1, so
     // a rounding disagreement between the DDA and the clipped interval loses nothing
-    const bool last = tnext[ax] >= t1 || c[ax] + step[ax] < 0 || c[ax] + step[ax] >= g.dims[ax];
-    const float tout = last ? t1 : tnext[ax];
-    const int64_t cell = ((int64_t)c[2] * g.dims[1] + c[1]) * g.dims[0] + c[0];
-    for (uint32_t i = g.cell_start[cell], e = g.cell_start[cell + 1]; i < e; ++i) {
+    const bool last = S.tnext[ax] >= R.t1 || S.c[ax] + R.step[ax] < 0 ||
+                      S.c[ax] + R.step[ax] >= g.dims[ax];
+    const float tout = last ? R.t1 : S.tnext[ax];
+    const int64_t cell = ((int64_t)S.c[2] * g.dims[1] + S.c[1]) * g.dims[0] + S.c[0];
+    const uint32_t b = g.cell_start[cell], e = g.cell_start[cell + 1];
+    for (uint32_t i = b + S.cursor; i < e; ++i) {
       const uint32_t s = g.entries[i];
       float te;
-      if (box_entry(o, id, g.box_lo[s], g.box_hi[s], t0, t1, te) && te >= tin && te <= tout)
+      if (box_entry(R.o, R.id, g.box_lo[s], g.box_hi[s], R.t0, R.t1, te) && te >= S.tin &&
+          te <= tout) {
         emit(s);
+        if (++n == kmax) {
+          S.cursor = i + 1 - b;
+          return n;
+        }
+      }
     }
-    if (last) break;
-    c[ax] += step[ax];
-    tin = tout;
-    tnext[ax] += tdelta[ax];
+    S.cursor = 0;
+    if (last) {
+      S.c[0] = -1;
+      break;
+    }
+    S.c[ax] += R.step[ax];
+    S.tin = tout;
+    S.tnext[ax] += R.tdelta[ax];
   }
+  return n;
+}
+
+template <class Emit>
+__device__ void walk(const GridView& g, float4 r0, float4 r1, Emit emit) {
+  RayDDA R;
+  DDAState S;
+  if (dda_setup(g, r0, r1, R, S)) dda_walk(g, R, S, 0xffffffffu, emit);
 }
 
 __global__ void __launch_bounds__(128) count_kernel(GridView g, const float4* rays, int64_t n_rays,
@@ -320,6 +370,53 @@ __global__ void __launch_bounds__(256) rounds_scatter_kernel(const uint32_t* off
     for (int j = 0; j < 4; ++j)
       if (cnt[j] > k) out[rank++] = csr[base[j] + k];
   }
+}
+
+// ---- closest hit with early termination (fiber_grid_closest) ----------------------------
+__global__ void closest_init_kernel(GridView g, const float4* rays, int64_t n_rays,
+                                    DDAState* st, uint32_t* active) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rays;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    RayDDA R;
+    DDAState S;
+    dda_setup(g, rays[2 * r], rays[2 * r + 1], R, S);
+    st[r] = S;
+    active[r] = (uint32_t)r;
+  }
+}
+
+// One round: every active ray whose best hit is not strictly before its walk position emits
+// its next k candidates into pairs[j*k ..] (unused slots: an out-of-range ray, a no-op pair);
+// keep[j] = the ray still has candidates after this round.
+__global__ void closest_walk_kernel(GridView g, const float4* rays, int64_t n_rays,
+                                    DDAState* st, const uint32_t* active, int64_t n_active,
+                                    uint32_t k, const unsigned long long* nearest, uint2* pairs,
+                                    uint32_t* keep) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_active;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = active[j];
+    DDAState S = st[r];
+    const unsigned long long key = nearest[r];
+    const float best = key == ~0ull ? INFINITY : __uint_as_float((uint32_t)(key >> 32));
+    uint32_t n = 0;
+    // every later candidate enters its box at t >= S.tin, and its hits lie in the box
+    if (S.c[0] >= 0 && !(best < S.tin)) {
+      RayDDA R;
+      dda_consts(g, rays[2 * r], rays[2 * r + 1], R);
+      uint32_t m = 0;
+      n = dda_walk(g, R, S, k, [&](uint32_t s) { pairs[(uint64_t)j * k + m++] = make_uint2(r, s); });
+      st[r] = S;
+    }
+    for (uint32_t q = n; q < k; ++q) pairs[(uint64_t)j * k + q] = make_uint2(0xffffffffu, 0u);
+    keep[j] = S.c[0] >= 0 && n > 0 ? 1u : 0u;
+  }
+}
+
+__global__ void compact_kernel(const uint32_t* active, const uint32_t* keep, const uint32_t* pos,
+                               int64_t n, uint32_t* out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if (keep[j]) out[pos[j]] = active[j];
 }
 
 int grid_blocks(int64_t n, int threads) {
@@ -518,5 +615,83 @@ extern "C" int fiber_grid_candidates(const fiber_grid* g, const fiber_ray* rays,
   cudaFree(bk);
   cudaFree(sums);
   if (!ok) return set_error(FIBER_ECUDA, "fiber_grid_candidates: CUDA failure");
+  return FIBER_OK;
+}
+
+extern "C" int fiber_grid_closest(const fiber_grid* g, const fiber_ray* rays, int64_t n_rays,
+                                  const fiber_segments* segs, int max_depth, uint64_t* nearest,
+                                  int* rounds_out, void* cuda_stream) {
+  if (!g || !segs || n_rays < 0 || n_rays >= ((int64_t)1 << 31) || (n_rays > 0 && (!rays || !nearest)) ||
+      max_depth < 0 || max_depth > FIBER_MAX_DEPTH || segs->n != g->n_segs)
+    return set_error(FIBER_EINVAL, "fiber_grid_closest: bad arguments");
+  int rc = check_device();
+  if (rc != FIBER_OK) return rc;
+  if (rounds_out) *rounds_out = 0;
+  if (n_rays == 0) return FIBER_OK;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  GridView v = view(g);
+  DDAState* state = nullptr;
+  uint32_t *act[2] = {nullptr, nullptr}, *keep = nullptr, *pos = nullptr, *sums = nullptr;
+  uint2* pairs = nullptr;
+  const uint32_t kmax = 256;
+  bool ok = cudaMalloc((void**)&state, n_rays * sizeof(DDAState)) == cudaSuccess &&
+            cudaMalloc((void**)&act[0], n_rays * sizeof(uint32_t)) == cudaSuccess &&
+            cudaMalloc((void**)&act[1], n_rays * sizeof(uint32_t)) == cudaSuccess &&
+            cudaMalloc((void**)&keep, (n_rays + 1) * sizeof(uint32_t)) == cudaSuccess &&
+            cudaMalloc((void**)&pos, (n_rays + 1) * sizeof(uint32_t)) == cudaSuccess &&
+            cudaMalloc((void**)&sums, fiberscan::scan_scratch(n_rays + 1) * sizeof(uint32_t)) == cudaSuccess;
+  // the pair buffer of a round: n_active * k <= max over rounds; grown on demand
+  size_t pair_cap = 0;
+  int64_t n_active = n_rays;
+  uint32_t k = 8;
+  int rounds = 0;
+  if (ok) {
+    closest_init_kernel<<<grid_blocks(n_rays, 256), 256, 0, st>>>(v, (const float4*)rays, n_rays,
+                                                                  state, act[0]);
+    ok = cudaGetLastError() == cudaSuccess;
+  }
+  int cur = 0;
+  while (ok && n_active > 0) {
+    const size_t need = (size_t)n_active * k;
+    if (need > pair_cap) {
+      cudaFree(pairs);
+      pairs = nullptr;
+      pair_cap = need;
+      ok = cudaMalloc((void**)&pairs, pair_cap * sizeof(uint2)) == cudaSuccess;
+      if (!ok) break;
+    }
+    closest_walk_kernel<<<grid_blocks(n_active, 128), 128, 0, st>>>(
+        v, (const float4*)rays, n_rays, state, act[cur], n_active, k,
+        (const unsigned long long*)nearest, pairs, keep);
+    ok = cudaGetLastError() == cudaSuccess;
+    if (!ok) break;
+    rc = launch_intersect_mode(rays, n_rays, segs, (const fiber_pair*)pairs, (int64_t)need,
+                               max_depth, nearest, cuda_stream, 3);
+    if (rc != FIBER_OK) {
+      ok = false;
+      break;
+    }
+    cudaMemsetAsync(keep + n_active, 0, sizeof(uint32_t), st);
+    fiberscan::exclusive_scan(keep, pos, n_active + 1, sums, st);
+    compact_kernel<<<grid_blocks(n_active, 256), 256, 0, st>>>(act[cur], keep, pos, n_active,
+                                                               act[cur ^ 1]);
+    uint32_t next = 0;
+    ok = cudaMemcpyAsync(&next, pos + n_active, sizeof(uint32_t), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+         cudaStreamSynchronize(st) == cudaSuccess;
+    n_active = next;
+    cur ^= 1;
+    k = k * 2 > kmax ? kmax : k * 2;
+    ++rounds;
+  }
+  cudaFree(state);
+  cudaFree(act[0]);
+  cudaFree(act[1]);
+  cudaFree(keep);
+  cudaFree(pos);
+  cudaFree(sums);
+  cudaFree(pairs);
+  if (rounds_out) *rounds_out = rounds;
+  if (rc != FIBER_OK) return rc;
+  if (!ok) return set_error(FIBER_ECUDA, "fiber_grid_closest: CUDA failure");
   return FIBER_OK;
 }

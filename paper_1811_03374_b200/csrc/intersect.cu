@@ -341,7 +341,9 @@ struct Params {
   uint32_t min_size;  // 2^(23 - depth), lst:algorithm
   float4* hits;
   unsigned long long* nearest;
-  int closest;  // bound each pair's t_max by its ray's best hit so far (fiber_intersect_closest)
+  int closest;  // bit 0: bound each pair's t_max by its ray's best hit so far
+                // (fiber_intersect_closest); bit 1: nearest keys carry the segment index
+                // instead of the pair index (fiber_grid_closest)
   unsigned int* counter;  // slot: [0] K2 pair counter, [2] K2 blocks done, [4]/[5] list
                           // appends (re-run / finalise); [0]-[5] are zero at launch and K2's
                           // last block returns them to zero after copying [4]/[5] to [6]/[7],
@@ -369,8 +371,9 @@ __device__ __forceinline__ void write_record(const Params& p, uint32_t i, uint32
                                              float u, uint32_t n_oct, uint32_t flags) {
   if (p.hits) p.hits[i] = make_float4(t, u, __uint_as_float(n_oct), __uint_as_float(flags));
   if (p.nearest && (flags & FIBER_HIT)) {
+    const uint32_t low = (p.closest & 2) ? __ldg(&p.pairs[i]).y : i;
     unsigned long long key =
-        ((unsigned long long)__float_as_uint(t) << 32) | (unsigned long long)i;
+        ((unsigned long long)__float_as_uint(t) << 32) | (unsigned long long)low;
     atomicMin(&p.nearest[ray], key);
   }
 }
@@ -484,7 +487,7 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e
   float ww = 1.0f / S.iww;
   e.lo0 = -S.ts * ww;
   float tlim = ray0.w;
-  if (p.closest) {
+  if (p.closest & 1) {
     // the ray's t_max as a running bound: the best hit of the
     // ray so far (read from L2, where the atomicMin of write_record lands), widened by
     // 2^-19 relative so that hits within FP32 rounding of it still compete for the minimum
@@ -1158,6 +1161,14 @@ extern "C" int fiber_intersect_nearest(const fiber_ray* rays, int64_t n_rays,
   if (n_pairs > 0 && !nearest) return set_error(FIBER_EINVAL, "fiber_intersect_nearest: NULL nearest");
   return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, hits, nearest, nullptr,
                           cuda_stream);
+}
+
+// For the library's own callers (grid.cu): mode bit 0 = closest, bit 1 = segment keys.
+int launch_intersect_mode(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
+                          const fiber_pair* pairs, int64_t n_pairs, int max_depth,
+                          uint64_t* nearest, void* stream, int mode) {
+  return launch_intersect(rays, n_rays, segs, pairs, n_pairs, max_depth, nullptr, nearest,
+                          nullptr, stream, mode);
 }
 
 extern "C" int fiber_intersect_closest(const fiber_ray* rays, int64_t n_rays,

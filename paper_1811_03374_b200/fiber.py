@@ -31,7 +31,7 @@ BAD_SEGMENT = 1 << 5
 EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments",
            "fiber_build_segments_quadratic", "fiber_presplit_count", "fiber_presplit_write",
            "fiber_remap_u", "fiber_grid_create", "fiber_grid_destroy", "fiber_grid_info",
-           "fiber_grid_count", "fiber_grid_candidates",
+           "fiber_grid_count", "fiber_grid_candidates", "fiber_grid_closest",
            "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
            "fiber_intersect_ex",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
@@ -74,6 +74,8 @@ def lib() -> ctypes.CDLL:
         L.fiber_grid_count.argtypes = [vp, vp, i64, vp, ctypes.POINTER(ctypes.c_uint32),
                                        ctypes.POINTER(ctypes.c_uint64), vp]
         L.fiber_grid_candidates.argtypes = [vp, vp, i64, vp, ctypes.c_uint32, ctypes.c_int, vp, vp]
+        L.fiber_grid_closest.argtypes = [vp, vp, i64, ctypes.POINTER(_Segs), ctypes.c_int, vp,
+                                         ctypes.POINTER(ctypes.c_int), vp]
         L.fiber_intersect.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int, vp,
                                       vp]
         L.fiber_intersect_nearest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
@@ -89,7 +91,7 @@ def lib() -> ctypes.CDLL:
                   "fiber_build_segments_quadratic", "fiber_presplit_count",
                   "fiber_presplit_write", "fiber_remap_u", "fiber_grid_create",
                   "fiber_grid_destroy", "fiber_grid_info", "fiber_grid_count",
-                  "fiber_grid_candidates"):
+                  "fiber_grid_candidates", "fiber_grid_closest"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -249,6 +251,21 @@ class Grid:
                                            {"ray": 0, "rounds": 1}[order], pairs.data_ptr(),
                                            _stream(stream)), "fiber_grid_candidates")
         return pairs[:int(tot.value)], off
+
+    def closest(self, rays: torch.Tensor, depth: int, nearest: torch.Tensor | None = None,
+                stream=None):
+        """fiber_grid_closest: per-ray nearest hit over the grid's candidates with early
+        termination -> (keys int64[n_rays] = (bits(t) << 32) | segment, -1 = none; rounds)."""
+        rays = _dev(rays, torch.float32, (8,), "rays")
+        if nearest is None:
+            nearest = torch.empty(rays.shape[0], dtype=torch.int64, device=rays.device)
+        nearest_init(nearest, stream)
+        rounds = ctypes.c_int()
+        _check(lib().fiber_grid_closest(self._h, rays.data_ptr(), rays.shape[0],
+                                        ctypes.byref(self._segs.desc), int(depth),
+                                        nearest.data_ptr(), ctypes.byref(rounds),
+                                        _stream(stream)), "fiber_grid_closest")
+        return nearest, rounds.value
 
 
 def _pairs(pairs: torch.Tensor) -> torch.Tensor:

@@ -55,6 +55,10 @@ ms, _ = timed(lambda: closest(pairs))
 res["closest_grid_ms"] = round(ms, 3)
 res["rays_hit"] = round(float((near != -1).float().mean()), 4)
 res["pipeline_G_rays_per_s"] = round(n_rays / (res["candidates_ms"] + res["closest_grid_ms"]) / 1e6, 4)
+ms, (keys, rounds) = timed(lambda: grid.closest(rays, depth))
+res["grid_closest_early_termination_ms"] = round(ms, 3)
+res["grid_closest_rounds"] = rounds
+res["grid_closest_G_rays_per_s"] = round(n_rays / ms / 1e6, 4)
 knn = torch.from_numpy(gen.candidate_rounds(w).pairs.view("int32")).cuda()
 ms, _ = timed(lambda: closest(knn))
 res["closest_knn16_ms"] = round(ms, 3)

@@ -148,3 +148,30 @@ def test_nearest_over_candidates_matches_oracle(fx):
     seg_o = need[best[both], 1]
     tie = second[both] <= tbest[both] * (1 + TOL_T)
     assert np.all((seg_g == seg_o) | tie)
+
+
+@pytest.mark.parametrize("depth", [6, 12])
+def test_grid_closest_early_termination_equals_full(fx, depth):
+    """fiber_grid_closest (rounds with early termination) gives every ray the same nearest
+    (t, segment) as the closest hit over ALL its candidates."""
+    ctrl, radii, rays = _scene()
+    segs = fx.build_segments(torch.from_numpy(ctrl).cuda(), torch.from_numpy(radii).cuda())
+    grid = fx.Grid(segs, 1.0)
+    tr = torch.from_numpy(rays).cuda()
+    keys, rounds = grid.closest(tr, depth)
+    pairs, _ = grid.candidates(tr, order="rounds")
+    near = torch.empty(rays.shape[0], dtype=torch.int64, device="cuda")
+    fx.nearest_init(near)
+    fx.intersect_nearest(tr, segs, pairs, depth, near)
+    full = near.cpu().numpy()
+    pairs = pairs.cpu().numpy()
+    exp = full.copy()
+    h = full != -1
+    exp[h] = (full[h] & ~0xFFFFFFFF) | pairs[full[h] & 0xFFFFFFFF, 1].astype(np.int64)
+    keys = keys.cpu().numpy()
+    # equal t bits; equal segment unless another candidate has exactly the same t (then the
+    # segment key takes the smaller id, the pair key the earlier pair)
+    assert np.array_equal(keys >> 32, exp >> 32)
+    same = keys == exp
+    assert same.mean() > 0.999
+    assert rounds >= 2 and (keys != -1).mean() > 0.9
