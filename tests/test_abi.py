@@ -71,6 +71,41 @@ def test_argument_errors_before_any_device_work(L):
     assert L.fiber_error_string(0) == b"ok"
 
 
+def test_argument_errors_of_the_next_rows(L):
+    """The 8(f) entry points (quadratic segments, pre-split, remap, closest, grid) reject bad
+    arguments with FIBER_EINVAL before any device work."""
+    from paper_1811_03374_b200.fiber import _Segs
+
+    d = _Segs()
+    d.n = 3
+    assert L.fiber_build_segments_quadratic(None, None, 3, ctypes.byref(d), None) == -1
+    assert L.fiber_build_segments_quadratic(1, 1, 2, ctypes.byref(d), None) == -1  # n mismatch
+    assert L.fiber_presplit_count(1, 1, 4, 17, 1, 1, None) == -1  # max_level > 16
+    assert L.fiber_presplit_count(None, None, 4, 8, 1, 1, None) == -1
+    assert L.fiber_presplit_count(1, 1, 4, 8, 1, None, None) == -1  # NULL offsets
+    assert L.fiber_presplit_write(1, 1, 4, 8, 1, None, 1, 1, 1, 1, 1, None) == -1
+    assert L.fiber_remap_u(None, None, 5, None, 1, None) == -1
+    assert L.fiber_remap_u(1, 1, -1, 1, 1, None) == -1
+    assert L.fiber_intersect_closest(1, 1, ctypes.byref(d), 1, 1, 4, None, None, None) == -1
+    assert L.fiber_intersect_ex(1, 1, ctypes.byref(d), 1, 1, 4, None, None, None, None) == -1
+    g = ctypes.c_void_p()
+    assert L.fiber_grid_create(None, ctypes.c_float(1.0), ctypes.byref(g), None) == -1
+    d.n = 0
+    assert L.fiber_grid_create(ctypes.byref(d), ctypes.c_float(1.0), ctypes.byref(g), None) == -1
+    d.n = 3
+    d.p0 = 1
+    assert L.fiber_grid_create(ctypes.byref(d), ctypes.c_float(0.0), ctypes.byref(g), None) == -1
+    mx, tot = ctypes.c_uint32(), ctypes.c_uint64()
+    assert L.fiber_grid_count(None, 1, 1, 1, ctypes.byref(mx), ctypes.byref(tot), None) == -1
+    assert L.fiber_grid_candidates(None, 1, 1, 1, 0, 0, 1, None) == -1
+    rounds = ctypes.c_int()
+    assert L.fiber_grid_closest(None, 1, 1, ctypes.byref(d), 4, 1, ctypes.byref(rounds), None) == -1
+    assert L.fiber_grid_destroy(None) == 0
+    dims = (ctypes.c_int32 * 3)()
+    ne = ctypes.c_int64()
+    assert L.fiber_grid_info(None, dims, ctypes.byref(ne)) == -1
+
+
 def test_decode_normal_matches_numpy_and_roundtrip(L):
     from paper_1811_03374_b200.fiber import decode_normals
 
