@@ -18,9 +18,15 @@
 
 namespace fiberx {
 
-constexpr int kThreads = 256;
+#ifndef FIBER_K2_THREADS
+#define FIBER_K2_THREADS 256
+#endif
+#ifndef FIBER_FAR_CACHE
+#define FIBER_FAR_CACHE 2
+#endif
+constexpr int kThreads = FIBER_K2_THREADS;
 constexpr int kWarps = kThreads / 32;
-constexpr int kFarCache = 2;  // per-lane cache of pending far children
+constexpr int kFarCache = FIBER_FAR_CACHE;  // per-lane cache of pending far children
 constexpr int kRingF4 = 5;  // a ring entry: the parent's Delta (4 float4) + its interval
 constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache) * kThreads * sizeof(float4) +
                                kThreads * sizeof(uint32_t);  // + the lanes' FP64 resume points
@@ -901,7 +907,11 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
       if (drained) break;
       continue;
     }
+#ifdef FIBER_UNROLL_EPOCH
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int k = 0; k < kEpoch; ++k) {
       if (active) {
 #ifdef FIBER_TRACE
