@@ -264,10 +264,15 @@ def run_ours(args):
 
 def e2e(args, fx, wls, dev):
     """Same metric through the public API with HOST buffers: every step copies each fiber's
-    rays, pairs and segment host->device (pinned) and every launch's hits device->host.
-    Pipelined as an application would: copies run on their own streams (both directions at
-    once) and overlap the launches -- the next fiber's inputs upload while this fiber's
-    depths run, and launch i's hits download while launch i+1 computes (two hit buffers)."""
+    rays, pairs and segment host->device (pinned) and brings every launch's result back to the
+    host: its hit records in pair order (fiber_compact_hits: the records with FIBER_HIT and
+    their pair indices; a pair without a hit carries no result) and their count.
+    Pipelined as an application would: copies run on their own streams and overlap the
+    launches -- the next fiber's inputs upload while this fiber's depths run, and launch i's
+    hits download while later launches compute (a ring of R result slots; the host reads
+    launch i's count L launches behind the compute it enqueues)."""
+    import collections
+
     import torch
 
     n = args.rays
@@ -281,20 +286,37 @@ def e2e(args, fx, wls, dev):
              torch.empty((n, 2), dtype=torch.int32, device=dev),
              torch.empty((1, 4, 3), dtype=torch.float32, device=dev),
              torch.empty((1, 4), dtype=torch.float32, device=dev)) for _ in range(nb)]
-    d_hits = [torch.empty((n, 4), dtype=torch.float32, device=dev) for _ in range(2)]
-    hits_h = [torch.empty((n, 4), dtype=torch.float32).pin_memory() for _ in range(2)]
+    d_hits = torch.empty((n, 4), dtype=torch.float32, device=dev)
+    R, LAG = 8, 4
+    d_out = [torch.empty((n, 4), dtype=torch.float32, device=dev) for _ in range(R)]
+    d_idx = [torch.empty((n,), dtype=torch.int32, device=dev) for _ in range(R)]
+    d_cnt = torch.zeros((R,), dtype=torch.int32, device=dev)
+    h_out = [torch.empty((n, 4), dtype=torch.float32).pin_memory() for _ in range(R)]
+    h_idx = [torch.empty((n,), dtype=torch.int32).pin_memory() for _ in range(R)]
+    h_cnt = torch.zeros((R,), dtype=torch.int32).pin_memory()
     comp = torch.cuda.current_stream()
     up, down = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ev_in = [torch.cuda.Event() for _ in range(nb)]
     ev_used = [torch.cuda.Event() for _ in range(nb)]  # inputs of fiber f consumed
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_free = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(R)]
+    ev_cnt = [torch.cuda.Event() for _ in range(R)]
+    ev_free = [torch.cuda.Event() for _ in range(R)]
     for e in ev_used + ev_free:
         e.record(comp)
-    counts = {"h2d": 0, "d2h": 0}
+    counts = {"h2d": 0, "d2h": 0, "hits": 0}
+
+    def drain(s):
+        ev_cnt[s].synchronize()  # this launch's count is on the host
+        k = int(h_cnt[s])
+        with torch.cuda.stream(down):
+            h_out[s][:k].copy_(d_out[s][:k], non_blocking=True)
+            h_idx[s][:k].copy_(d_idx[s][:k], non_blocking=True)
+            ev_free[s].record(down)
+        counts["d2h"] += 4 + 20 * k
+        counts["hits"] += k
 
     def step():
-        counts["h2d"] = counts["d2h"] = 0
+        counts["h2d"] = counts["d2h"] = counts["hits"] = 0
         with torch.cuda.stream(up):  # all uploads of the step, in order, on the copy stream
             for f, (r, p, c, ra) in enumerate(host):
                 up.wait_event(ev_used[f])
@@ -302,23 +324,29 @@ def e2e(args, fx, wls, dev):
                     dst.copy_(src, non_blocking=True)
                     counts["h2d"] += src.numel() * 4
                 ev_in[f].record(up)
+        pending = collections.deque()
         j = 0
         for f in range(nb):
             comp.wait_event(ev_in[f])
             d_rays, d_pairs, d_ctrl, d_rad = d_in[f]
             segs = fx.build_segments(d_ctrl, d_rad)
             for D in DEPTHS:
-                b = j & 1
-                comp.wait_event(ev_free[b])
-                fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits[b])
-                ev_done[b].record(comp)
+                s = j % R
+                comp.wait_event(ev_free[s])  # slot s's previous result is on the host
+                fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits)
+                fx.compact_hits(d_hits, out=d_out[s], idx=d_idx[s], count=d_cnt[s:s + 1])
+                ev_done[s].record(comp)
                 with torch.cuda.stream(down):
-                    down.wait_event(ev_done[b])
-                    hits_h[b].copy_(d_hits[b], non_blocking=True)
-                    ev_free[b].record(down)
-                counts["d2h"] += d_hits[b].numel() * 4
+                    down.wait_event(ev_done[s])
+                    h_cnt[s:s + 1].copy_(d_cnt[s:s + 1], non_blocking=True)
+                    ev_cnt[s].record(down)
+                pending.append(s)
+                if len(pending) > LAG:
+                    drain(pending.popleft())
                 j += 1
             ev_used[f].record(comp)
+        while pending:
+            drain(pending.popleft())
         comp.wait_stream(down)  # the step ends when its last hits are on the host
         return counts["h2d"], counts["d2h"]
 
@@ -337,7 +365,10 @@ def e2e(args, fx, wls, dev):
     return {"value": round(tests / (ms * 1e-3) / 1e9, 4), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(ms / k, 3), "steps": k,
-            "note": "copies on two copy streams overlapping the launches (double-buffered hits)"}
+            "hits_per_step": int(counts["hits"]),
+            "note": "results = per launch the hit records in pair order + their pair indices "
+                    "(fiber_compact_hits) + the count; copies on two copy streams overlapping "
+                    "the launches (ring of 8 result slots)"}
 
 
 # ------------------------------------------------------------------------------- oracle

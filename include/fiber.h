@@ -270,6 +270,22 @@ int fiber_intersect_ex(const fiber_ray *rays, int64_t n_rays, const fiber_segmen
                        const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
                        uint64_t *nearest, void *event_after_traverse, void *cuda_stream);
 
+/* Order-preserving stream compaction of hit records, for callers that move only the hits
+ * off the device (the problem statement returns "the nearest intersection or nothing",
+ * P:251-257, so a pair without FIBER_HIT carries no result).
+ *   hits   device fiber_hit[n], as written by fiber_intersect / _ex (complete: call after them
+ *          on the same stream)
+ *   n      number of records, 0 <= n < 2^32
+ *   out    device fiber_hit[n] (worst case): out[k] = hits[idx[k]], k < *count
+ *   idx    device uint32[n] or NULL: idx[k] = the pair index of the k-th hit, increasing
+ *   count  device uint32[1]: the number of records with FIBER_HIT
+ * Deterministic (the k-th hit in pair order goes to slot k).  Scratch comes from the
+ * library's stream-ordered pool.  Asynchronous like fiber_intersect.
+ * Errors: FIBER_EINVAL (n out of range, count NULL, hits/out NULL with n > 0),
+ * FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_compact_hits(const fiber_hit *hits, int64_t n, fiber_hit *out, uint32_t *idx,
+                       uint32_t *count, void *cuda_stream);
+
 /* Fill nearest[0..n_rays) with the "no hit" key (all ones). */
 int fiber_nearest_init(uint64_t *nearest, int64_t n_rays, void *cuda_stream);
 

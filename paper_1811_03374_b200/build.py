@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "segments.cu", "intersect.cu", "presplit.cu", "grid.cu"]
+SOURCES = ["api.cu", "segments.cu", "intersect.cu", "presplit.cu", "grid.cu", "compact.cu"]
 HEADERS = ["fiber_device.cuh", "fiber_internal.h", "exact.cuh", "gatekeeper.cuh", "scan.cuh"]
 LIB = os.path.join(HERE, "libfiber.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -99,4 +99,4 @@ extern "C" void fiber_decode_normal(uint32_t n_oct, float out[3]) {
   out[2] = z / l;
 }
 
-extern "C" int fiber_abi_version(void) { return 100; }
+extern "C" int fiber_abi_version(void) { return 101; }

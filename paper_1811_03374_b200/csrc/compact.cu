@@ -1,0 +1,106 @@
+// compact.cu -- fiber_compact_hits: order-preserving stream compaction of hit records.
+//
+// A renderer consumes only the pairs that hit (the query returns the nearest
+// intersection "or nothing"), so the records worth moving off the device are the hits.  Two
+// passes over the records with the three-phase scan of scan.cuh: per-tile hit counts, a
+// scan of the tile counts, then each tile writes its hits at their global rank.  The result
+// is deterministic: out[k] is the record of the k-th hit pair in pair order.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "fiber.h"
+#include "fiber_internal.h"
+#include "scan.cuh"
+
+namespace fibercompact {
+
+using fiberscan::kPer;
+using fiberscan::kThreads;
+using fiberscan::kTile;
+
+// thread t of tile b owns records b*kTile + t*kPer .. +kPer-1 (contiguous, so ranks follow
+// pair order)
+__device__ __forceinline__ uint32_t tile_hits(const uint4* hits, int64_t n, int64_t base,
+                                              uint32_t& mask) {
+  uint32_t s = 0;
+  mask = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if (base + k < n && (__ldg(&hits[base + k].w) & FIBER_HIT)) {
+      mask |= 1u << k;
+      ++s;
+    }
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(kThreads) count_kernel(const uint4* __restrict__ hits, int64_t n,
+                                                        uint32_t* __restrict__ sums,
+                                                        int64_t tiles) {
+  const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kPer;
+  uint32_t mask;
+  uint32_t total;
+  fiberscan::block_excl(tile_hits(hits, n, base, mask), &total);
+  if (threadIdx.x == 0) {
+    sums[blockIdx.x] = total;
+    if (blockIdx.x == 0) sums[tiles] = 0u;  // the scan's last element becomes the total
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const uint4* __restrict__ hits, int64_t n,
+                                                          const uint32_t* __restrict__ sums,
+                                                          int64_t tiles, uint4* __restrict__ out,
+                                                          uint32_t* __restrict__ idx,
+                                                          uint32_t* __restrict__ count) {
+  const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kPer;
+  uint32_t mask;
+  uint32_t total;
+  uint32_t run = fiberscan::block_excl(tile_hits(hits, n, base, mask), &total) + sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if (mask & (1u << k)) {
+      out[run] = __ldg(&hits[base + k]);
+      if (idx) idx[run] = (uint32_t)(base + k);
+      ++run;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = sums[tiles];
+}
+
+}  // namespace fibercompact
+
+extern "C" int fiber_compact_hits(const fiber_hit* hits, int64_t n, fiber_hit* out, uint32_t* idx,
+                                  uint32_t* count, void* cuda_stream) {
+  if (n < 0 || n >= ((int64_t)1 << 32) || !count || (n > 0 && (!hits || !out)))
+    return set_error(FIBER_EINVAL, "fiber_compact_hits: bad size or NULL pointer");
+  int rc = check_device();
+  if (rc != FIBER_OK) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (n == 0) {
+    if (cudaMemsetAsync(count, 0, sizeof(uint32_t), st) != cudaSuccess)
+      return check_launch("fiber_compact_hits (memset)");
+    return FIBER_OK;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = scratch_pool(dev);
+  const int64_t tiles = (n + fibercompact::kTile - 1) / fibercompact::kTile;
+  uint32_t* sums = nullptr;
+  cudaError_t e = pool ? cudaMallocFromPoolAsync((void**)&sums, (tiles + 1) * sizeof(uint32_t), pool, st)
+                       : cudaErrorMemoryAllocation;
+  if (e != cudaSuccess) {
+    char buf[300];
+    snprintf(buf, sizeof(buf), "fiber_compact_hits: scratch: %s", cudaGetErrorString(e));
+    return set_error(FIBER_ECUDA, buf);
+  }
+  fibercompact::count_kernel<<<(unsigned)tiles, fibercompact::kThreads, 0, st>>>(
+      (const uint4*)hits, n, sums, tiles);
+  fiberscan::scan_sums<<<1, 1024, 0, st>>>(sums, tiles + 1);
+  fibercompact::scatter_kernel<<<(unsigned)tiles, fibercompact::kThreads, 0, st>>>(
+      (const uint4*)hits, n, sums, tiles, (uint4*)out, idx, count);
+  rc = check_launch("fiber_compact_hits");
+  cudaFreeAsync(sums, st);
+  return rc;
+}

@@ -15,3 +15,6 @@ int check_launch(const char* what);
 int launch_intersect_mode(const fiber_ray* rays, int64_t n_rays, const fiber_segments* segs,
                           const fiber_pair* pairs, int64_t n_pairs, int max_depth,
                           uint64_t* nearest, void* stream, int mode);
+// The library's private stream-ordered scratch pool of device `dev` (intersect.cu): keeps its
+// memory between calls, so per-call scratch needs no system calls after warm-up.
+cudaMemPool_t scratch_pool(int dev);

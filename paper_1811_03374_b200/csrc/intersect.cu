@@ -1068,7 +1068,7 @@ static float4* g_trace_buf = nullptr;
 // The per-call scratch (two work lists of n_pairs entries, and records when the caller
 // gives none) comes from a private stream-ordered memory pool per device that keeps its
 // memory (no system calls after warm-up, no effect on the application's default pool).
-static cudaMemPool_t scratch_pool(int dev) {
+cudaMemPool_t scratch_pool(int dev) {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
   std::lock_guard<std::mutex> lock(mu);

@@ -1,12 +1,13 @@
 // scan.cuh -- device-wide exclusive prefix sum of uint32 (three phases: block sums, a
 // single-block scan of the block sums, block scans plus the block prefix).  Used by the
-// candidate generator (grid.cu).  In-place allowed.
+// candidate generator (grid.cu) and the hit compaction (compact.cu).  In-place allowed.
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 namespace fiberscan {
+namespace {  // internal linkage: every translation unit that includes this gets its own kernels
 
 constexpr int kThreads = 256, kPer = 4, kTile = kThreads * kPer;  // 1024 elements per block
 
@@ -109,4 +110,5 @@ inline void exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_
 
 inline int64_t scan_scratch(int64_t n) { return (n + kTile - 1) / kTile; }
 
+}  // namespace
 }  // namespace fiberscan

@@ -33,7 +33,7 @@ EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments"
            "fiber_remap_u", "fiber_grid_create", "fiber_grid_destroy", "fiber_grid_info",
            "fiber_grid_count", "fiber_grid_candidates", "fiber_grid_closest",
            "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
-           "fiber_intersect_ex",
+           "fiber_intersect_ex", "fiber_compact_hits",
            "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
 
 
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
         L.fiber_intersect_closest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
                                               ctypes.c_int, vp, vp, vp]
         L.fiber_nearest_init.argtypes = [vp, i64, vp]
+        L.fiber_compact_hits.argtypes = [vp, i64, vp, vp, vp, vp]
         L.fiber_intersect_ex.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int,
                                          vp, vp, vp, vp]
         for f in ("fiber_segments_view", "fiber_build_segments", "fiber_intersect",
@@ -91,7 +92,7 @@ def lib() -> ctypes.CDLL:
                   "fiber_build_segments_quadratic", "fiber_presplit_count",
                   "fiber_presplit_write", "fiber_remap_u", "fiber_grid_create",
                   "fiber_grid_destroy", "fiber_grid_info", "fiber_grid_count",
-                  "fiber_grid_candidates", "fiber_grid_closest"):
+                  "fiber_grid_candidates", "fiber_grid_closest", "fiber_compact_hits"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -341,6 +342,27 @@ def intersect_closest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, d
                                          nearest.data_ptr(), _stream(stream)),
            "fiber_intersect_closest")
     return nearest
+
+
+def compact_hits(hits: torch.Tensor, out: torch.Tensor | None = None,
+                 idx: torch.Tensor | None = None, count: torch.Tensor | None = None,
+                 with_idx: bool = True, stream=None):
+    """fiber_compact_hits: (out f32[n,4], idx i32[n] or None, count i32[1]) on the device;
+    out[:count] are the records with FIBER_HIT in pair order, idx[:count] their pair indices."""
+    hits = _dev(hits, torch.float32, (4,), "hits")
+    n = hits.shape[0]
+    if out is None:
+        out = torch.empty((n, 4), dtype=torch.float32, device=hits.device)
+    if idx is None and with_idx:
+        idx = torch.empty((n,), dtype=torch.int32, device=hits.device)
+    if count is None:
+        count = torch.empty((1,), dtype=torch.int32, device=hits.device)
+    if out.shape[0] < n or (idx is not None and idx.numel() < n):
+        raise FiberError("compact_hits: out / idx must hold n records")
+    _check(lib().fiber_compact_hits(hits.data_ptr(), n, out.data_ptr(),
+                                    idx.data_ptr() if idx is not None else None,
+                                    count.data_ptr(), _stream(stream)), "fiber_compact_hits")
+    return out, idx, count
 
 
 def nearest_init(nearest: torch.Tensor, stream=None) -> torch.Tensor:

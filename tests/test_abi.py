@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol(L):
     assert set(names) == set(fiber.EXPORTS)
     for n in names:
         assert hasattr(L, n), n
-    assert L.fiber_abi_version() == 100
+    assert L.fiber_abi_version() == 101
 
 
 def test_segments_bytes_and_view(L):
@@ -67,6 +67,12 @@ def test_argument_errors_before_any_device_work(L):
     assert L.fiber_build_segments(None, None, 4, ctypes.byref(d), None) == -1  # n mismatch
     assert L.fiber_build_segments(None, None, 5, ctypes.byref(d), None) == -1  # NULLs
     assert L.fiber_nearest_init(None, 3, None) == -1
+    # hit compaction: NULL count, negative / oversized n, NULL records with n > 0
+    assert L.fiber_compact_hits(1, 4, 1, None, None, None) == -1
+    assert L.fiber_compact_hits(1, -1, 1, None, 1, None) == -1
+    assert L.fiber_compact_hits(1, 1 << 32, 1, None, 1, None) == -1
+    assert L.fiber_compact_hits(None, 4, 1, None, 1, None) == -1
+    assert L.fiber_compact_hits(1, 4, None, None, 1, None) == -1
     assert b"NULL" in L.fiber_error_string(-1) or b"bad" in L.fiber_error_string(-1)
     assert L.fiber_error_string(0) == b"ok"
 
