@@ -353,6 +353,9 @@ def e2e(args, fx, wls, dev):
     for _ in range(2):
         step()
     torch.cuda.synchronize()
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
     k = max(1, min(args.steps, 3))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
@@ -361,7 +364,14 @@ def e2e(args, fx, wls, dev):
     e1.record(comp)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    tests = n * len(FIBERS) * len(DEPTHS) * k
+    world = 1
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        # whole-job number: every rank's tests over the slowest rank's time
+        world = torch.distributed.get_world_size()
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    tests = world * n * len(FIBERS) * len(DEPTHS) * k
     return {"value": round(tests / (ms * 1e-3) / 1e9, 4), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(ms / k, 3), "steps": k,
