@@ -146,3 +146,42 @@ def test_full_size_config2_sampled(fx, fiber):
     # property at any size: hit fraction as the oracle's sample, counters non-zero
     assert abs(g["hit"].mean() - o["hit"].mean()) < 0.02
     assert (g["tests"] >= 1).all()
+
+
+@pytest.mark.parametrize("depth", [6, 12])
+def test_config5_fur_parity(fx, depth):
+    """C5 recipe (fur on the unit sphere, 16 kNN candidates per targeted ray) at a reduced
+    strand count: 4,096 strands x 4 segments, 2^13 rays x 16 = 2^17 pairs."""
+    w = gen.config5(n_rays=1 << 13, n_strands=1 << 12, depth=depth)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+    assert rep["hits"] > 1000
+
+
+def _sampled(fx, w, n_sample, seed, **kw):
+    """The full launch on the GPU; a seeded sample of its pairs through the oracle."""
+    g = _run(fx, w)
+    sub = np.sort(np.random.default_rng(seed).choice(w.n_pairs, n_sample, replace=False))
+    o = oracle.intersect(w.rays, w.ctrl, w.radii, w.pairs[sub], w.depth)
+    gs = {k: (v[sub] if isinstance(v, np.ndarray) else v) for k, v in g.items()}
+    rep = compare(gs, o)
+    assert_parity(rep, **kw)
+    assert (g["tests"] >= 1).all()
+    return g, o, rep
+
+
+def test_full_size_config3_sampled(fx):
+    """C3 at its BASELINE size (2^20 rays x 16 candidates = 2^24 pairs, D = 9), one launch;
+    an 8192-pair sample compared with the oracle pair by pair."""
+    w = gen.config3()
+    g, o, rep = _sampled(fx, w, 8192, 31)
+    assert abs(g["hit"].mean() - o["hit"].mean()) < 0.02
+
+
+def test_full_size_config4_sampled(fx):
+    """C4 at its BASELINE size (2^24 thin-fiber pairs, D = 22, half grazing), one launch; an
+    8192-pair sample compared with the oracle (grazing-band exclusions as the subsampled
+    test)."""
+    w = gen.config4()
+    g, o, rep = _sampled(fx, w, 8192, 41, max_excluded_frac=0.1)
+    assert abs(g["hit"].mean() - o["hit"].mean()) < 0.02

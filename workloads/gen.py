@@ -114,6 +114,10 @@ def thick_ok(P: np.ndarray, rbar: np.ndarray, samples: int = 256,
     if end_samples:
         e = 2.0 ** -np.arange(1, end_samples + 1)
         u = np.sort(np.r_[u, e, 1.0 - e])
+    chunk = max(1, (1 << 22) // len(u))  # bounded temporaries for large segment sets
+    if P.shape[0] > chunk:
+        return np.concatenate([thick_ok(P[a:a + chunk], rbar[a:a + chunk], samples, end_samples)
+                               for a in range(0, P.shape[0], chunk)])
     X = bezier(P[:, None, :, :3], u[None, :])             # [n, s, 3]
     T = _unit(bezier_tangent(P[:, None, :, :3], u[None, :]))
     ok = np.ones(P.shape[0], dtype=bool)
@@ -402,19 +406,21 @@ def _validate(segs: np.ndarray, radii: np.ndarray):
     the five constraints, |t0|, |t1| >= 0.05 |d|, and the sampled thick-fiber check.
     A violating segment is straightened towards its chord until valid."""
     segs = segs.copy()
+    todo = np.arange(segs.shape[0])  # segments not yet known valid (a valid one is never changed)
     for it in range(8):
-        m = constraint_margins(segs)
-        d = np.linalg.norm(segs[:, 3] - segs[:, 0], axis=1)
-        t0 = np.linalg.norm(segs[:, 1] - segs[:, 0], axis=1)
-        t1 = np.linalg.norm(segs[:, 3] - segs[:, 2], axis=1)
+        sg = segs[todo]
+        m = constraint_margins(sg)
+        d = np.linalg.norm(sg[:, 3] - sg[:, 0], axis=1)
+        t0 = np.linalg.norm(sg[:, 1] - sg[:, 0], axis=1)
+        t1 = np.linalg.norm(sg[:, 3] - sg[:, 2], axis=1)
         ok = (m.min(1) >= 1e-3 * d * d) & (t0 >= 0.05 * d) & (t1 >= 0.05 * d)
-        ok &= thick_ok(segs, radii.max(1))
+        ok &= thick_ok(sg, radii[todo].max(1))
         if ok.all():
             break
-        bad = ~ok
-        lin = segs[bad, 0][:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None, :, None] * (
-            segs[bad, 3] - segs[bad, 0])[:, None]
-        segs[bad] = 0.5 * segs[bad] + 0.5 * lin
+        todo = todo[~ok]
+        lin = segs[todo, 0][:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None, :, None] * (
+            segs[todo, 3] - segs[todo, 0])[:, None]
+        segs[todo] = 0.5 * segs[todo] + 0.5 * lin
     return segs.astype(np.float32), radii.astype(np.float32)
 
 
