@@ -268,8 +268,10 @@ def e2e(args, fx, wls, dev):
     host: its hit records in pair order (fiber_compact_hits: the records with FIBER_HIT and
     their pair indices; a pair without a hit carries no result) and their count.
     Pipelined as an application would: copies run on their own streams and overlap the
-    launches -- the next fiber's inputs upload while this fiber's depths run, and launch i's
-    hits download while later launches compute (a ring of R result slots; the host reads
+    launches, and the 63 independent launches alternate between two compute streams (the
+    library is stream-safe), so one launch's latency-bound FP64 tail (K3) overlaps the next
+    launch's traversal.  The next fiber's inputs upload while this fiber's depths run; launch
+    i's hits download while later launches compute (a ring of R result slots; the host reads
     launch i's count L launches behind the compute it enqueues)."""
     import collections
 
@@ -282,11 +284,12 @@ def e2e(args, fx, wls, dev):
                      torch.from_numpy(w.pairs.view(np.int32)).pin_memory(),
                      torch.from_numpy(w.ctrl).pin_memory(), torch.from_numpy(w.radii).pin_memory()))
     nb = len(host)
+    NC = 2  # compute streams
     d_in = [(torch.empty((n, 8), dtype=torch.float32, device=dev),
              torch.empty((n, 2), dtype=torch.int32, device=dev),
              torch.empty((1, 4, 3), dtype=torch.float32, device=dev),
              torch.empty((1, 4), dtype=torch.float32, device=dev)) for _ in range(nb)]
-    d_hits = torch.empty((n, 4), dtype=torch.float32, device=dev)
+    d_hits = [torch.empty((n, 4), dtype=torch.float32, device=dev) for _ in range(NC)]
     R, LAG = 8, 4
     d_out = [torch.empty((n, 4), dtype=torch.float32, device=dev) for _ in range(R)]
     d_idx = [torch.empty((n,), dtype=torch.int32, device=dev) for _ in range(R)]
@@ -294,15 +297,16 @@ def e2e(args, fx, wls, dev):
     h_out = [torch.empty((n, 4), dtype=torch.float32).pin_memory() for _ in range(R)]
     h_idx = [torch.empty((n,), dtype=torch.int32).pin_memory() for _ in range(R)]
     h_cnt = torch.zeros((R,), dtype=torch.int32).pin_memory()
-    comp = torch.cuda.current_stream()
+    main = torch.cuda.current_stream()
+    comps = [torch.cuda.Stream(device=dev) for _ in range(NC)]
     up, down = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ev_in = [torch.cuda.Event() for _ in range(nb)]
-    ev_used = [torch.cuda.Event() for _ in range(nb)]  # inputs of fiber f consumed
+    ev_used = [[torch.cuda.Event() for _ in range(NC)] for _ in range(nb)]  # fiber f consumed
     ev_done = [torch.cuda.Event() for _ in range(R)]
     ev_cnt = [torch.cuda.Event() for _ in range(R)]
     ev_free = [torch.cuda.Event() for _ in range(R)]
-    for e in ev_used + ev_free:
-        e.record(comp)
+    for e in [x for row in ev_used for x in row] + ev_free:
+        e.record(main)
     counts = {"h2d": 0, "d2h": 0, "hits": 0}
 
     def drain(s):
@@ -317,25 +321,38 @@ def e2e(args, fx, wls, dev):
 
     def step():
         counts["h2d"] = counts["d2h"] = counts["hits"] = 0
+        for c in comps + [up, down]:
+            c.wait_stream(main)
         with torch.cuda.stream(up):  # all uploads of the step, in order, on the copy stream
             for f, (r, p, c, ra) in enumerate(host):
-                up.wait_event(ev_used[f])
+                for e in ev_used[f]:
+                    up.wait_event(e)
                 for dst, src in zip(d_in[f], (r, p, c, ra)):
                     dst.copy_(src, non_blocking=True)
                     counts["h2d"] += src.numel() * 4
                 ev_in[f].record(up)
         pending = collections.deque()
+        keep = []  # every Segments of the step stays alive until the step is over
         j = 0
         for f in range(nb):
-            comp.wait_event(ev_in[f])
             d_rays, d_pairs, d_ctrl, d_rad = d_in[f]
-            segs = fx.build_segments(d_ctrl, d_rad)
+            segs = None
             for D in DEPTHS:
-                s = j % R
-                comp.wait_event(ev_free[s])  # slot s's previous result is on the host
-                fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits)
-                fx.compact_hits(d_hits, out=d_out[s], idx=d_idx[s], count=d_cnt[s:s + 1])
-                ev_done[s].record(comp)
+                s, cs = j % R, comps[j % NC]
+                with torch.cuda.stream(cs):
+                    cs.wait_event(ev_in[f])
+                    if segs is None:
+                        segs = fx.build_segments(d_ctrl, d_rad, stream=cs)
+                        keep.append(segs)
+                        ev_seg = torch.cuda.Event()
+                        ev_seg.record(cs)
+                    else:
+                        cs.wait_event(ev_seg)
+                    cs.wait_event(ev_free[s])  # slot s's previous result is on the host
+                    fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits[j % NC], stream=cs)
+                    fx.compact_hits(d_hits[j % NC], out=d_out[s], idx=d_idx[s],
+                                    count=d_cnt[s:s + 1], stream=cs)
+                    ev_done[s].record(cs)
                 with torch.cuda.stream(down):
                     down.wait_event(ev_done[s])
                     h_cnt[s:s + 1].copy_(d_cnt[s:s + 1], non_blocking=True)
@@ -344,10 +361,12 @@ def e2e(args, fx, wls, dev):
                 if len(pending) > LAG:
                     drain(pending.popleft())
                 j += 1
-            ev_used[f].record(comp)
+            for c, e in zip(comps, ev_used[f]):
+                e.record(c)
         while pending:
             drain(pending.popleft())
-        comp.wait_stream(down)  # the step ends when its last hits are on the host
+        for c in comps + [down]:  # the step ends when its last hits are on the host
+            main.wait_stream(c)
         return counts["h2d"], counts["d2h"]
 
     for _ in range(2):
@@ -358,10 +377,10 @@ def e2e(args, fx, wls, dev):
         torch.cuda.synchronize()
     k = max(1, min(args.steps, 3))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(comp)
+    e0.record(main)
     for _ in range(k):
         h2d, d2h = step()
-    e1.record(comp)
+    e1.record(main)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     world = 1
@@ -377,8 +396,8 @@ def e2e(args, fx, wls, dev):
             "ms_per_step": round(ms / k, 3), "steps": k,
             "hits_per_step": int(counts["hits"]),
             "note": "results = per launch the hit records in pair order + their pair indices "
-                    "(fiber_compact_hits) + the count; copies on two copy streams overlapping "
-                    "the launches (ring of 8 result slots)"}
+                    "(fiber_compact_hits) + the count; launches alternate between 2 compute "
+                    "streams, copies on two copy streams overlapping them (ring of 8 result slots)"}
 
 
 # ------------------------------------------------------------------------------- oracle
