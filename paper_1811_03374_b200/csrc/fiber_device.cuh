@@ -21,14 +21,51 @@ namespace fiberx {
 __device__ __forceinline__ float4 f4(float x, float y, float z, float w) {
   return make_float4(x, y, z, w);
 }
+// Packed FP32 (sm_100 FFMA2 / FADD2 / FMUL2): one issue slot for two lanes' worth of the
+// float4 arithmetic of the descent; a scalar operand is broadcast by the instruction.
+// -DFIBER_NO_PACKED builds the scalar form (a test build).
+#ifndef FIBER_NO_PACKED
+#define FIBER_PACKED 1
+__device__ __forceinline__ float2 lo2(float4 a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ float2 hi2(float4 a) { return make_float2(a.z, a.w); }
+__device__ __forceinline__ float4 cat2(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+__device__ __forceinline__ float2 s2(float s) { return make_float2(s, s); }
+// a * b + c, a a scalar
+__device__ __forceinline__ float4 fma4(float a, float4 b, float4 c) {
+  return cat2(__ffma2_rn(s2(a), lo2(b), lo2(c)), __ffma2_rn(s2(a), hi2(b), hi2(c)));
+}
+__device__ __forceinline__ float4 mul4(float a, float4 b) {
+  return cat2(__fmul2_rn(s2(a), lo2(b)), __fmul2_rn(s2(a), hi2(b)));
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return cat2(__fadd2_rn(lo2(a), lo2(b)), __fadd2_rn(hi2(a), hi2(b)));
+}
+__device__ __forceinline__ float4 sub4(float4 a, float4 b) {
+  return cat2(__ffma2_rn(s2(-1.0f), lo2(b), lo2(a)), __ffma2_rn(s2(-1.0f), hi2(b), hi2(a)));
+}
+#endif
+
+// float4 arithmetic: packed where available (fma(-1, b, a) rounds exactly as a - b)
 __device__ __forceinline__ float4 operator+(float4 a, float4 b) {
+#ifdef FIBER_PACKED
+  return add4(a, b);
+#else
   return f4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+#endif
 }
 __device__ __forceinline__ float4 operator-(float4 a, float4 b) {
+#ifdef FIBER_PACKED
+  return sub4(a, b);
+#else
   return f4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+#endif
 }
 __device__ __forceinline__ float4 operator*(float s, float4 a) {
+#ifdef FIBER_PACKED
+  return mul4(s, a);
+#else
   return f4(s * a.x, s * a.y, s * a.z, s * a.w);
+#endif
 }
 __device__ __forceinline__ float dot3(float4 a, float4 b) {
   return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z));
@@ -223,9 +260,15 @@ struct Split {
 
 // Split point and tangent of node c (3.1): delta_p, t_c and S = p + delta_p.
 __device__ __forceinline__ void split_geometry(const Delta& c, Split& sp) {
+#ifdef FIBER_PACKED
+  sp.dp = fma4(0.375f, sub4(c.t0, c.t1), mul4(0.5f, c.d));
+  sp.tcn = fma4(-0.125f, add4(c.t0, c.t1), mul4(0.25f, c.d));
+  sp.S = add4(c.p, sp.dp);
+#else
   sp.dp = 0.375f * (c.t0 - c.t1) + 0.5f * c.d;
   sp.tcn = 0.25f * c.d - 0.125f * (c.t0 + c.t1);
   sp.S = c.p + sp.dp;
+#endif
 }
 
 __device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, float& tmin,
@@ -249,8 +292,19 @@ __device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, f
   return sp;
 }
 
-// The child on side `right` of the split (selects only).
+// The child on side `right` of the split.  Packed form: blends with r = 0 / 1 that are
+// exact for finite operands (x + 0 y = x, 0 x + y = y, 1 x + y = fl(x + y)), so the child
+// equals the selected one up to the sign of a zero:
+//   p'  = p + r dp,   d' = (1 - 2r) dp + r d,
+//   t0' = (1-r)/2 t0 + r t_c,   t1' = r/2 t1 + (1 - r) t_c.
 __device__ __forceinline__ void child(const Delta& c, const Split& sp, bool right, Delta& out) {
+#ifdef FIBER_PACKED
+  const float r = right ? 1.0f : 0.0f, nr = 1.0f - r;
+  out.p = fma4(r, sp.dp, c.p);
+  out.d = fma4(fmaf(-2.0f, r, 1.0f), sp.dp, mul4(r, c.d));
+  out.t0 = fma4(0.5f * nr, c.t0, mul4(r, sp.tcn));
+  out.t1 = fma4(0.5f * r, c.t1, mul4(nr, sp.tcn));
+#else
 #define FX_SEL4(dst, a, b)                                                             \
   dst = make_float4(right ? (a).x : (b).x, right ? (a).y : (b).y, right ? (a).z : (b).z, \
                     right ? (a).w : (b).w)
@@ -260,6 +314,7 @@ __device__ __forceinline__ void child(const Delta& c, const Split& sp, bool righ
   FX_SEL4(out.t0, sp.tcn, h0);
   FX_SEL4(out.t1, h1, sp.tcn);
 #undef FX_SEL4
+#endif
 }
 
 }  // namespace fiberx

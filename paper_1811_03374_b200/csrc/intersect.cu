@@ -386,7 +386,15 @@ __device__ __forceinline__ void write_record(const Params& p, uint32_t i, uint32
 
 // world vector v (xyz, w = radius part) -> local frame (no translation)
 __device__ __forceinline__ float4 rot(const Setup32& S, const float4 w, float4 v) {
+#ifdef FIBER_PACKED
+  // (<v,b1>, <v,b2>) as one packed dot product, in dot3's order of operations
+  const float2 xy = __ffma2_rn(s2(v.x), make_float2(S.b1.x, S.b2.x),
+                               __ffma2_rn(s2(v.y), make_float2(S.b1.y, S.b2.y),
+                                          __fmul2_rn(s2(v.z), make_float2(S.b1.z, S.b2.z))));
+  return make_float4(xy.x, xy.y, dot3(v, w), v.w);
+#else
   return make_float4(dot3(v, S.b1), dot3(v, S.b2), dot3(v, w), v.w);
+#endif
 }
 
 // ------------------------------------------------------------------------------------
