@@ -937,6 +937,9 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
     }
   }
   if (ended != ST_RUNNING) end_pair(p, pair, L, ended, badseg, hs);
+  // this warp has no pairs left: K3 (a programmatic dependent) may be scheduled once every
+  // block got here; it still waits for K2's completion before reading anything
+  asm volatile("griddepcontrol.launch_dependents;");
   // the last block publishes the list lengths for K3 in slot words 6-7 (stable until the
   // slot's next use) and returns the slot's working words to zero
   __syncthreads();
@@ -997,6 +1000,9 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   // warp with no divergence; a re-run that hits is finalised by the same lane.  No atomics:
   // both lists are dealt statically from the lengths K2's last block published.
   const uint32_t lane = threadIdx.x & 31u;
+  // launched as a programmatic dependent of K2 (launch_intersect): wait until K2 has
+  // completed and its memory (records, lists, list lengths) is visible
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t n_exact = p.counter[6];
   const uint32_t n_fin = p.counter[7];
   const uint32_t W = gridDim.x * (blockDim.x >> 5);
@@ -1157,7 +1163,23 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   if (rc == FIBER_OK && event_after_traverse) cudaEventRecord((cudaEvent_t)event_after_traverse, st);
   if (rc == FIBER_OK) {
     const int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
-    finalize_kernel<<<(unsigned)fblocks, kK3Threads, 0, st>>>(p);
+    // Programmatic dependent launch: K3's launch is processed while K2 drains, and K3 waits
+    // for K2's completion on the device (griddepcontrol.wait) -- not with an event in between
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)fblocks);
+    cfg.blockDim = dim3(kK3Threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifdef FIBER_NO_PDL  // test build: plain stream order
+    attr[0].val.programmaticStreamSerializationAllowed = 0;
+#else
+    attr[0].val.programmaticStreamSerializationAllowed = event_after_traverse ? 0 : 1;
+#endif
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, finalize_kernel, p);
     rc = check_launch("fiber_intersect (finalize)");
   }
   cudaFreeAsync(scratch, st);
