@@ -219,6 +219,23 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
         right = num < 0.0;
         both = false;
       }
+#ifndef FIBER_K3_SELECT
+      // the child as an exact blend with r = 0 / 1 (as K2's child(); no divergent copies of
+      // the loop-carried curve): p' = p + r dp, d' = (1 - 2r) dp + r d,
+      // t0' = (1-r)/2 t0 + r t_c, t1' = r/2 t1 + (1-r) t_c
+      {
+        const double r = right ? 1.0 : 0.0, nr = 1.0 - r, s = 1.0 - 2.0 * r;
+        const double h0 = 0.5 * nr, h1 = 0.5 * r;
+        auto blend = [](double a, V4 x, V4 y) {  // a x + y
+          return v4(fma(a, x.x, y.x), fma(a, x.y, y.y), fma(a, x.z, y.z), fma(a, x.w, y.w));
+        };
+        const V4 d = cur.d;
+        cur.p = blend(r, dp, cur.p);
+        cur.d = blend(s, dp, scl(r, d));
+        cur.t0 = blend(h0, cur.t0, scl(r, tcn));
+        cur.t1 = blend(h1, cur.t1, scl(nr, tcn));
+      }
+#else
       if (right) {
         cur.p = S;
         cur.d = sub(cur.d, dp);
@@ -229,6 +246,7 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
         cur.t0 = scl(0.5, cur.t0);
         cur.t1 = tcn;
       }
+#endif
       size >>= 1;
       if (both) bits |= size;
       if (right) start |= size;
