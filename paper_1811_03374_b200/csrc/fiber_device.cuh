@@ -271,27 +271,6 @@ __device__ __forceinline__ void split_geometry(const Delta& c, Split& sp) {
 #endif
 }
 
-__device__ __forceinline__ Split partition(const Delta& c, float c0, float c1, float& tmin,
-                                           float& tmax, uint32_t& tag, bool crop, uint32_t umid,
-                                           bool& right, bool& both, float& tP, float& kappa) {
-  Split sp;
-  split_geometry(c, sp);
-  float num = dot3(sp.tcn, sp.S), nz = sp.tcn.z;
-  float rz = frcp(nz);
-  tP = num * rz;
-  kappa = fminf((fabsf(sp.tcn.x) + fabsf(sp.tcn.y) + fabsf(nz)) * fabsf(rz), 1e30f);
-  bool par = (nz == 0.0f);
-  right = par ? (num < 0.0f) : ((tP > c0) != (nz > 0.0f));
-  both = !par && (c0 < tP) && (tP < c1);
-  bool up = tP > c0;
-  bool apply = crop && !par;
-  tmax = (apply && up) ? fminf(tmax, tP) : tmax;
-  bool lo_up = apply && !up && (tP > tmin);
-  tmin = lo_up ? tP : tmin;
-  tag = lo_up ? umid : tag;
-  return sp;
-}
-
 // The child on side `right` of the split.  Packed form: blends with r = 0 / 1 that are
 // exact for finite operands (x + 0 y = x, 0 x + y = y, 1 x + y = fl(x + y)), so the child
 // equals the selected one up to the sign of a zero:
