@@ -350,7 +350,7 @@ struct Params {
   int closest;  // bit 0: bound each pair's t_max by its ray's best hit so far
                 // (fiber_intersect_closest); bit 1: nearest keys carry the segment index
                 // instead of the pair index (fiber_grid_closest)
-  unsigned int* counter;  // slot: [0] K2 pair counter, [2] K2 blocks done, [4]/[5] list
+  unsigned int* counter;  // slot: [0-1] K2 pair counter (64-bit), [2] K2 blocks done, [4]/[5] list
                           // appends (re-run / finalise); [0]-[5] are zero at launch and K2's
                           // last block returns them to zero after copying [4]/[5] to [6]/[7],
                           // the list lengths K3 reads (so a slot needs no memset between calls)
@@ -462,8 +462,7 @@ struct Prepared {
 
 // a2: transform pair i's segment into its ray frame (lst:transform_curve P:1482-1512) and
 // form the root interval.  Returns false for bad input (written as a miss).
-__device__ __forceinline__ bool prepare(const Params& p, uint32_t i, Prepared& e) {
-  const uint2 pr = __ldg(&p.pairs[i]);
+__device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2 pr, Prepared& e) {
   if ((int64_t)pr.x >= p.n_rays || (int64_t)pr.y >= p.n_segs) {
     write_record(p, i, 0, INFINITY, 0.0f, 0u, FIBER_BAD_INPUT);
     return false;
@@ -885,6 +884,8 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
   uint32_t pair = 0, badseg = 0;
   int ended = ST_RUNNING;  // a finished pair whose record is not written yet
   bool active = false, drained = false;
+  // The pair counter is 64-bit (slot words 0-1): claims past n_pairs cannot wrap.
+  unsigned long long* const pair_counter = reinterpret_cast<unsigned long long*>(p.counter);
   while (true) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (!drained && (__popc(idle) >= (int)kRefill || idle == 0xffffffffu)) {
@@ -894,15 +895,20 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
         end_pair(p, pair, L, ended, badseg, hs);
         ended = ST_RUNNING;
       }
+      const uint32_t k = __popc(idle), r = __popc(idle & lt);
       uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&p.counter[0], (uint32_t)__popc(idle));
+      if (lane == 0) {
+        const unsigned long long b = atomicAdd(pair_counter, (unsigned long long)k);
+        base = (uint32_t)min(b, (unsigned long long)p.n_pairs);
+      }
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (base + (uint32_t)__popc(idle) >= p.n_pairs) drained = true;
+      if (base + k >= p.n_pairs) drained = true;
       if (!active) {
-        const uint32_t i = base + __popc(idle & lt);
+        const uint32_t i = base + r;
         if (i < p.n_pairs) {
+          const uint2 pr = __ldg(&p.pairs[i]);
           Prepared e;
-          if (prepare(p, i, e)) {  // a2
+          if (prepare(p, i, pr, e)) {  // a2
             start_lane(e, L, hs);
             pair = e.pair;
             badseg = e.badseg;
@@ -949,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
       __threadfence();
       p.counter[6] = atomicExch(&p.counter[4], 0u);
       p.counter[7] = atomicExch(&p.counter[5], 0u);
-      atomicExch(&p.counter[0], 0u);
+      atomicExch(pair_counter, 0ull);
       atomicExch(&p.counter[2], 0u);
     }
   }
