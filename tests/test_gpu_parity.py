@@ -185,3 +185,14 @@ def test_full_size_config4_sampled(fx):
     w = gen.config4()
     g, o, rep = _sampled(fx, w, 8192, 41, max_excluded_frac=0.1)
     assert abs(g["hit"].mean() - o["hit"].mean()) < 0.02
+
+
+@pytest.mark.parametrize("n_rays", [1, 31, 33, 1037])
+@pytest.mark.parametrize("depth", [0, 1, 23])
+def test_ragged_sizes_and_extreme_depths(fx, n_rays, depth):
+    """Pair counts that are not a multiple of the warp width (a ragged last warp, a launch
+    smaller than one warp) at the ends of the depth range: D = 0 (the root is the leaf),
+    D = 1 and D = 23 (min_size = 1, the 23-bit limit of the bit string)."""
+    w = gen.config2("B", n_rays=n_rays, depth=depth, targeted=True)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
