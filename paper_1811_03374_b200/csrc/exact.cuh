@@ -1,4 +1,4 @@
-// exact.cuh -- the traversal in FP64 (kernel K4), for the pairs the FP32 traversal (K2)
+// exact.cuh -- the traversal in FP64 (run by kernel K3), for the pairs the FP32 traversal (K2)
 // flagged as decided by a near-tie (R5).
 //
 // The same algorithm as K2 (lst:algorithm P:1591-1651 with F1-F9), written in double: the
@@ -16,17 +16,27 @@
 namespace fiberx {
 namespace exact {
 
-// Double-precision reciprocal and square root from the MUFU seeds (rcp/rsqrt.approx.f64)
-// refined by two Newton steps: ~1 ulp, and a short dependency chain instead of the IEEE
-// division/sqrt sequences (the FP64 path is latency-bound: a re-run is one lane's chain).
+// Double-precision reciprocal, division and square root from the MUFU seeds
+// (rcp/rsqrt.approx.f64) refined by Newton steps: ~1 ulp, and a short dependency chain
+// instead of the IEEE division/sqrt sequences (a re-run is one lane's latency-bound chain).
+// rcp64 takes two steps.
 __device__ __forceinline__ double rcp64(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   r = fma(r, fma(-x, r, 1.0), r);
   return fma(r, fma(-x, r, 1.0), r);
 }
+// The seeds are good to 2^-20 (measured on B200: scripts/micro/seed.cu).  One Newton step
+// gives ~1e-12; the residual correction that ends div64 and sqrt64 squares that error, so
+// both need only one step before it (FIBER_K3_NEWTON2 builds the two-step form).
 __device__ __forceinline__ double div64(double a, double b) {
+#ifdef FIBER_K3_NEWTON2
   const double r = rcp64(b);
+#else
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  r = fma(r, fma(-b, r, 1.0), r);
+#endif
   const double q = a * r;
   return fma(r, fma(-b, q, a), q);  // one residual correction
 }
@@ -35,7 +45,9 @@ __device__ __forceinline__ double sqrt64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   y = y * fma(-0.5 * x * y, y, 1.5);
+#ifdef FIBER_K3_NEWTON2
   y = y * fma(-0.5 * x * y, y, 1.5);
+#endif
   const double s = x * y;
   return fma(0.5 * y, fma(-s, s, x), s);
 }
