@@ -28,7 +28,12 @@ constexpr int kThreads = FIBER_K2_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kFarCache = FIBER_FAR_CACHE;  // per-lane cache of pending far children
 constexpr int kRingF4 = 5;  // a ring entry: the parent's Delta (4 float4) + its interval
-constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache) * kThreads * sizeof(float4) +
+#ifndef FIBER_NO_RAYSTASH
+constexpr int kRayStash = 1;  // per-lane copy of the ray direction + ray index (end_pair)
+#else
+constexpr int kRayStash = 0;
+#endif
+constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache + kRayStash) * kThreads * sizeof(float4) +
                                kThreads * sizeof(uint32_t);  // + the lanes' FP64 resume points
 
 // ------------------------------------------------------------------------------------
@@ -421,6 +426,7 @@ struct HodoRef {
   float4* base;  // hodograph slot: &smem[threadIdx.x]
   float4* far;   // parent ring:    &smem[4 * kThreads + threadIdx.x]
   uint32_t* rs;  // FP64 resume point (start | log2(size) << 24), written at the first tie
+  float4* wr;    // the pair's ray direction (xyz) and ray index (w bits), written at setup
   __device__ __forceinline__ void push(const Delta& f, float4 ival, uint32_t slot) const {
     float4* q = far + slot * kRingF4 * kThreads;
     q[0] = f.p;
@@ -462,7 +468,8 @@ struct Prepared {
 
 // a2: transform pair i's segment into its ray frame (lst:transform_curve P:1482-1512) and
 // form the root interval.  Returns false for bad input (written as a miss).
-__device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2 pr, Prepared& e) {
+__device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2 pr, Prepared& e,
+                                        float4* wr) {
   if ((int64_t)pr.x >= p.n_rays || (int64_t)pr.y >= p.n_segs) {
     write_record(p, i, 0, INFINITY, 0.0f, 0u, FIBER_BAD_INPUT);
     return false;
@@ -472,6 +479,7 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2
   const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
   const float4 P2 = __ldg(&p.p2[pr.y]), P3 = __ldg(&p.p3[pr.y]);
   const uint32_t sf = __ldg(&p.sflags[pr.y]);
+  if (kRayStash) *wr = make_float4(ray1.x, ray1.y, ray1.z, __uint_as_float(pr.x));
   e.badseg = (sf & FIBER_SEG_INVALID_MASK) != 0u ? FIBER_BAD_SEGMENT : 0u;
   e.pair = i;
   Setup32 S;
@@ -738,8 +746,13 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
       // and the FP32 coordinate error is far below the radius (normal error ~ delta / r);
       // otherwise a provisional record for K3's FP64 re-solve
       if (!inside && p.depth <= FIBER_FP32_FIN_DEPTH && L.delta < 1.220703125e-4f * L.cur.p.w) {
+#ifndef FIBER_NO_RAYSTASH
+        const float4 w = *hs.wr;  // stashed at setup: no dependent pair -> ray reload
+        const uint2 pr = make_uint2(__float_as_uint(w.w), 0u);
+#else
         const uint2 pr = __ldg(&p.pairs[i]);
         const float4 w = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
+#endif
         const float sign = copysignf(1.0f, w.z);
         const float a = -frcp(sign + w.z), b = w.x * w.y * a;
         const float4 b1 = make_float4(fmaf(sign * w.x * w.x, a, 1.0f), sign * b, -sign * w.x, 0.f);
@@ -878,7 +891,8 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
   HodoRef hs{&smem[threadIdx.x], &smem[4 * kThreads + threadIdx.x],
-             reinterpret_cast<uint32_t*>(&smem[(4 + kRingF4 * kFarCache) * kThreads]) + threadIdx.x};
+             reinterpret_cast<uint32_t*>(&smem[(4 + kRingF4 * kFarCache) * kThreads]) + threadIdx.x,
+             &smem[(4 + kRingF4 * kFarCache) * kThreads + kThreads / 4 + threadIdx.x]};
   const uint32_t min_size = p.min_size;
   Lane L;
   uint32_t pair = 0, badseg = 0;
@@ -908,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
         if (i < p.n_pairs) {
           const uint2 pr = __ldg(&p.pairs[i]);
           Prepared e;
-          if (prepare(p, i, pr, e)) {  // a2
+          if (prepare(p, i, pr, e, hs.wr)) {  // a2
             start_lane(e, L, hs);
             pair = e.pair;
             badseg = e.badseg;
