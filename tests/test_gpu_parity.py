@@ -59,6 +59,17 @@ def test_config2_parity_depth_sweep(fx, fiber, depth):
     assert_parity(rep)
 
 
+@pytest.mark.parametrize("fiber", ["A", "B", "C"])
+@pytest.mark.parametrize("depth", [5, 7, 8, 10, 11, 13, 14, 15, 17, 18, 19, 21])
+def test_config2_parity_remaining_depths(fx, fiber, depth):
+    # with the sweep above, every depth 2-22 of the metric (BASELINE.json north_star) is
+    # compared against the oracle for all three fibers
+    w = gen.config2(fiber, n_rays=1 << 13, depth=depth)
+    rep = compare(_run(fx, w), _oracle(w))
+    assert_parity(rep)
+    assert rep["hits"] > 100
+
+
 @pytest.mark.parametrize("depth", [4, 9, 22])
 def test_config2_targeted_parity(fx, depth):
     w = gen.config2("A", n_rays=1 << 14, depth=depth, targeted=True)
