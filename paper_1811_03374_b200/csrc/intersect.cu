@@ -1031,7 +1031,11 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
 #ifdef FIBER_K3_PACKED  // diagnostic: 32 consecutive re-runs per warp
   for (uint32_t k = gw * 32u + lane; k < n_exact; k += W * 32u) {
 #else
-  for (uint32_t k = gw + W * lane; k < n_exact; k += W * 32u) {
+#ifndef FIBER_K3_DEAL  // >0: deal the re-runs over only enough warps for ~this many per warp
+#define FIBER_K3_DEAL 0
+#endif
+  const uint32_t We = FIBER_K3_DEAL > 0 ? max(1u, min(W, (n_exact + FIBER_K3_DEAL - 1u) / FIBER_K3_DEAL)) : W;
+  for (uint32_t k = gw + We * lane; gw < We && k < n_exact; k += We * 32u) {
 #endif
     const uint32_t i = p.list_exact[k];
     exact_one(p, i);  // the FP64 traversal, then the finalisation if it hit
@@ -1182,7 +1186,10 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   rc = check_launch("fiber_intersect (traverse)");
   if (rc == FIBER_OK && event_after_traverse) cudaEventRecord((cudaEvent_t)event_after_traverse, st);
   if (rc == FIBER_OK) {
-    const int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
+#ifndef FIBER_K3_GRID  // K3 blocks per SM launched (0: as many as fit)
+#define FIBER_K3_GRID 0
+#endif
+    const int64_t fblocks = (int64_t)li->sms * (FIBER_K3_GRID > 0 ? std::min(FIBER_K3_GRID, li->k3_per_sm) : li->k3_per_sm);
     // Programmatic dependent launch: K3's launch is processed while K2 drains, and K3 waits
     // for K2's completion on the device (griddepcontrol.wait) -- not with an event in between
     cudaLaunchConfig_t cfg = {};
