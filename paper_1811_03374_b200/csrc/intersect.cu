@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <atomic>
+#include <chrono>
+#include <unistd.h>
 #include <mutex>
 
 #include "fiber.h"
@@ -359,8 +361,17 @@ struct Params {
                           // appends (re-run / finalise); [0]-[5] are zero at launch and K2's
                           // last block returns them to zero after copying [4]/[5] to [6]/[7],
                           // the list lengths K3 reads (so a slot needs no memset between calls)
+#ifdef FIBER_K3_STREAM
+  // K3 streams the lists while K2 drains: an entry is (seq << 32) | pair, stored with release
+  // semantics after the pair's record, so stale pool memory (other seq) reads as not-ready;
+  // K2's last block stores seq in counter[3] after publishing the lengths in [6]/[7]
+  unsigned long long* list_exact;
+  unsigned long long* list_fin;
+  uint32_t seq;  // unique per call (never 0)
+#else
   uint32_t* list_exact;   // pairs K2 flagged for the FP64 re-run   [n_pairs]
   uint32_t* list_fin;     // provisional hits for the FP64 finalise [n_pairs]
+#endif
 #ifdef FIBER_TRACE
   uint32_t trace_pair;  // test build only: per-iteration records of one pair
   float4* trace;        // [kTraceCap] x 3 float4
@@ -712,6 +723,18 @@ __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
   }
 }
 
+#ifdef FIBER_K3_STREAM
+__device__ __forceinline__ void list_append(unsigned long long* list, uint32_t k, uint32_t i,
+                                            const Params& p) {
+  const unsigned long long e = ((unsigned long long)p.seq << 32) | i;
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(list + k), "l"(e) : "memory");
+}
+#else
+__device__ __forceinline__ void list_append(uint32_t* list, uint32_t k, uint32_t i, const Params&) {
+  list[k] = i;
+}
+#endif
+
 __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
   return (min(L.backtracks, 255u) << 8) | (min(L.tests, 65535u) << 16);
 }
@@ -727,7 +750,7 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
   if (L.tie) {  // decided by a near-tie somewhere: K3 re-runs the pair in FP64
     p.hits[i] = make_float4(__uint_as_float(*hs.rs), __uint_as_float(L.tie & 31u),
                             __uint_as_float(L.tie & ~31u), __uint_as_float(badseg | kUncertain));
-    p.list_exact[atomicAdd(&p.counter[4], 1u)] = i;
+    list_append(p.list_exact, atomicAdd(&p.counter[4], 1u), i, p);
     return;
   }
   if (st == ST_HIT) {
@@ -797,7 +820,7 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
       p.hits[i] = make_float4(zs, __uint_as_float(L.start | (kind << 24) | (inside << 26)),
                               __uint_as_float(L.tag),
                               __uint_as_float(counter_bits(L) | badseg | kProvisional));
-      p.list_fin[atomicAdd(&p.counter[5], 1u)] = i;
+      list_append(p.list_fin, atomicAdd(&p.counter[5], 1u), i, p);
       return;
     }
   }
@@ -916,7 +939,13 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
         base = (uint32_t)min(b, (unsigned long long)p.n_pairs);
       }
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (base + k >= p.n_pairs) drained = true;
+      if (base + k >= p.n_pairs) {
+        drained = true;
+#ifdef FIBER_K3_STREAM
+        // every pair is claimed: K3 may become resident as K2 blocks exit and stream the lists
+        asm volatile("griddepcontrol.launch_dependents;");
+#endif
+      }
       if (!active) {
         const uint32_t i = base + r;
         if (i < p.n_pairs) {
@@ -971,6 +1000,10 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
       p.counter[7] = atomicExch(&p.counter[5], 0u);
       atomicExch(pair_counter, 0ull);
       atomicExch(&p.counter[2], 0u);
+#ifdef FIBER_K3_STREAM
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&p.counter[3]), "r"(p.seq) : "memory");
+#endif
     }
   }
 }
@@ -1020,6 +1053,65 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   // warp with no divergence; a re-run that hits is finalised by the same lane.  No atomics:
   // both lists are dealt statically from the lengths K2's last block published.
   const uint32_t lane = threadIdx.x & 31u;
+#ifdef FIBER_K3_STREAM
+  // no griddepcontrol.wait: K3 starts while K2 drains and takes each list entry once it is
+  // published (tagged with this call's seq); an index is past the end once K2's last block
+  // has stored seq in counter[3] and the published length says so
+  const uint32_t W = gridDim.x * (blockDim.x >> 5);
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t seq = p.seq;
+  // 1 = item in *item, 0 = past the end, -1 = not known yet
+  auto probe = [&](const unsigned long long* list, uint32_t k, int len_word, uint32_t* item) -> int {
+    if (k >= p.n_pairs) return 0;
+    const unsigned long long e = *(const volatile unsigned long long*)(list + k);
+    if ((uint32_t)(e >> 32) == seq) {
+      *item = (uint32_t)e;
+      return 1;
+    }
+    if (*(const volatile uint32_t*)&p.counter[3] == seq) {
+      __threadfence();
+      if (k >= *(const volatile uint32_t*)&p.counter[len_word]) return 0;
+      const unsigned long long e2 = *(const volatile unsigned long long*)(list + k);
+      if ((uint32_t)(e2 >> 32) == seq) {
+        *item = (uint32_t)e2;
+        return 1;
+      }
+    }
+    return -1;
+  };
+  // the whole warp waits until every lane knows its entry, then runs converged
+  auto take = [&](const unsigned long long* list, uint32_t k, int len_word, uint32_t* item) -> int {
+    int r = probe(list, k, len_word, item);
+    while (__any_sync(0xffffffffu, r < 0)) {
+      if (r < 0) {
+        __nanosleep(256);
+        r = probe(list, k, len_word, item);
+      }
+    }
+    __threadfence();  // acquire: the records behind the entries are visible
+    return r;
+  };
+#ifndef FIBER_NO_EXACT
+  for (uint32_t k0 = gw;; k0 += W * 32u) {
+    uint32_t i = 0;
+    const int r = take(p.list_exact, k0 + W * lane, 6, &i);
+    if (r == 1) {
+      exact_one(p, i);
+      if (__float_as_uint(p.hits[i].w) & kProvisional) finalize_one(p, i);
+    }
+    if (__all_sync(0xffffffffu, r == 0)) break;
+  }
+#endif
+#ifndef FIBER_NO_FIN
+  for (uint32_t c = W - 1u - gw;; c += W) {
+    uint32_t i = 0;
+    const int r = take(p.list_fin, c * 32u + lane, 7, &i);
+    if (r == 1) finalize_one(p, i);
+    if (__all_sync(0xffffffffu, r == 0)) break;
+  }
+#endif
+}
+#else
   // launched as a programmatic dependent of K2 (launch_intersect): wait until K2 has
   // completed and its memory (records, lists, list lengths) is visible
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1049,6 +1141,7 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
     if (c * 32u + lane < n_fin) finalize_one(p, p.list_fin[c * 32u + lane]);
 #endif
 }
+#endif  // FIBER_K3_STREAM
 
 __global__ void fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1143,9 +1236,14 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   cudaGetDevice(&dev);
   cudaMemPool_t pool = scratch_pool(dev);
   // work counters: a self-resetting slot of the per-device pool
-  unsigned int* counter = li->slots + kSlotWords * (g_next_slot.fetch_add(1u) % kSlots);
+  const unsigned call_no = g_next_slot.fetch_add(1u);
+  unsigned int* counter = li->slots + kSlotWords * (call_no % kSlots);
   // the lists first, the records (16-B float4 stores) at the next 256-B boundary
+#ifdef FIBER_K3_STREAM
+  const size_t list_bytes = (2 * (size_t)n_pairs * sizeof(unsigned long long) + 255) & ~(size_t)255;
+#else
   const size_t list_bytes = (2 * (size_t)n_pairs * sizeof(uint32_t) + 255) & ~(size_t)255;
+#endif
   const size_t rec_bytes = hits ? 0 : (size_t)n_pairs * sizeof(fiber_hit);
   void* scratch = nullptr;
   cudaError_t e = pool ? cudaMallocFromPoolAsync(&scratch, list_bytes + rec_bytes, pool, st)
@@ -1177,8 +1275,18 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   p.nearest = (unsigned long long*)nearest;
   p.closest = closest;
   p.counter = counter;
+#ifdef FIBER_K3_STREAM
+  p.list_exact = (unsigned long long*)scratch;
+  p.list_fin = (unsigned long long*)scratch + n_pairs;
+  // salted per process, so list memory left by another process cannot carry a matching tag
+  static const unsigned salt =
+      ((unsigned)std::chrono::steady_clock::now().time_since_epoch().count() * 2654435761u) ^
+      (unsigned)getpid();
+  p.seq = (salt + call_no) == 0u ? 1u : salt + call_no;
+#else
   p.list_exact = (uint32_t*)scratch;
   p.list_fin = (uint32_t*)scratch + n_pairs;
+#endif
   int64_t chunks = (n_pairs + 31) / 32;
   int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
   if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
