@@ -11,12 +11,12 @@
  *
  * Conventions for every call:
  *   - Pointers marked "device" are CUDA device pointers owned by the caller.  The library
- *     keeps, per device and per process, immutable launch constants, a pool of 1024
- *     self-resetting work-counter slots (so at most 1024 calls may be in flight on one
- *     device at once) and a private stream-ordered memory pool from which each
- *     fiber_intersect call takes 8 bytes per pair of scratch (work lists; 16 more per pair
- *     when no hits buffer is given) and returns it on the same stream.  It is re-entrant
- *     and thread-safe.
+ *     keeps, per device and per process, immutable launch constants and a private
+ *     stream-ordered memory pool from which each fiber_intersect call takes its scratch
+ *     (its own work counters, zeroed on its stream, and work lists: 256 B + 8 B per pair;
+ *     16 B more per pair when no hits buffer is given) and returns it on the same stream.
+ *     No state is shared between calls, so any number may be in flight on any streams.
+ *     It is re-entrant and thread-safe.
  *   - Work is enqueued on `cuda_stream` (a cudaStream_t, NULL = legacy default stream) and
  *     the call returns immediately; outputs are valid after that stream synchronises, and
  *     inputs must not change before then.  Kernel faults surface at the next sync.

@@ -28,15 +28,11 @@ __device__ __forceinline__ double rcp64(double x) {
 }
 // The seeds are good to 2^-20 (measured on B200: scripts/micro/seed.cu).  One Newton step
 // gives ~1e-12; the residual correction that ends div64 and sqrt64 squares that error, so
-// both need only one step before it (FIBER_K3_NEWTON2 builds the two-step form).
+// both need only one step before it.
 __device__ __forceinline__ double div64(double a, double b) {
-#ifdef FIBER_K3_NEWTON2
-  const double r = rcp64(b);
-#else
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   r = fma(r, fma(-b, r, 1.0), r);
-#endif
   const double q = a * r;
   return fma(r, fma(-b, q, a), q);  // one residual correction
 }
@@ -45,9 +41,6 @@ __device__ __forceinline__ double sqrt64(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   y = y * fma(-0.5 * x * y, y, 1.5);
-#ifdef FIBER_K3_NEWTON2
-  y = y * fma(-0.5 * x * y, y, 1.5);
-#endif
   const double s = x * y;
   return fma(0.5 * y, fma(-s, s, x), s);
 }
@@ -231,7 +224,6 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
         right = num < 0.0;
         both = false;
       }
-#ifndef FIBER_K3_SELECT
       // the child as an exact blend with r = 0 / 1 (as K2's child(); no divergent copies of
       // the loop-carried curve): p' = p + r dp, d' = (1 - 2r) dp + r d,
       // t0' = (1-r)/2 t0 + r t_c, t1' = r/2 t1 + (1-r) t_c
@@ -247,18 +239,6 @@ __device__ __forceinline__ Result traverse(const float4 ray0, const float4 ray1,
         cur.t0 = blend(h0, cur.t0, scl(r, tcn));
         cur.t1 = blend(h1, cur.t1, scl(nr, tcn));
       }
-#else
-      if (right) {
-        cur.p = S;
-        cur.d = sub(cur.d, dp);
-        cur.t0 = tcn;
-        cur.t1 = scl(0.5, cur.t1);
-      } else {
-        cur.d = dp;
-        cur.t0 = scl(0.5, cur.t0);
-        cur.t1 = tcn;
-      }
-#endif
       size >>= 1;
       if (both) bits |= size;
       if (right) start |= size;

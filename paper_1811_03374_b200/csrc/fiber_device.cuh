@@ -98,6 +98,12 @@ __device__ __forceinline__ float frcp(float x) {
 }
 __device__ __forceinline__ float fdiv(float a, float b) { return a * frcp(b); }
 #endif
+// 1/sqrt(x) to ~1 ulp: the MUFU seed and one Newton step (unit ray directions, a2 setup)
+__device__ __forceinline__ float frsqrt(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y * fmaf(-0.5f * x * y, y, 1.5f);
+}
 
 // ------------------------------------------------------------------------------------
 // Curve in the (p, d, t0, t1) representation of 3.1, FP32.

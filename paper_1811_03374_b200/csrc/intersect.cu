@@ -302,40 +302,49 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
 // ------------------------------------------------------------------------------------
 // a2 setup: FP32 frame with an FP64-exact origin shift
 // ------------------------------------------------------------------------------------
-// The frame origin o' = o + ts w is placed on the ray next to the segment anchor
-// c = fl((P0 + P3) / 2).  Local coordinates of a point X are (<X-o', b1>, <X-o', b2>,
-// <X-o', w>) with (b1, b2) the FP32 Duff/Frisvad basis of w.  They are split as
-// <X - c, b> (small, FP32) + rho, rho = <c - o - ts w, b>: rho carries the cancellation of
-// |c - o| ~ |ray length| and is formed in FP64 from the exact FP32 inputs, so every local
-// coordinate is accurate to FP32 rounding of the SEGMENT's size.  The ray is then the unit
-// ray (0,0,0) + z (0,0,1) of P:475-481 with z = (t - ts) |w|^2.
+// The frame origin o' = o + ts d is placed on the ray next to the segment anchor
+// c = fl((P0 + P3) / 2) (ts: the ray parameter along d as given).  With w^ = d / |d| (FP32,
+// ~1 ulp) and (b1, b2) the FP32 Duff/Frisvad basis of w^, local coordinates of
+// a point X are (<X-o', b1>, <X-o', b2>, <X-o', w^>).  They are split as <X - c, b> (small,
+// FP32) + rho, rho = <c - o - ts d, b>: rho carries the cancellation of |c - o| ~ |ray
+// length| and is formed in FP64 from the exact FP32 inputs, so every local coordinate is
+// accurate to FP32 rounding of the SEGMENT's size.  The ray is then the unit ray
+// (0,0,0) + z (0,0,1) of P:475-481 with z = (t - ts) |d|; t = (z - lo0) / |d|, lo0 = -ts |d|.
 struct Setup32 {
-  float4 b1, b2;  // xyz used
-  float ts, iww;
+  float4 b1, b2, wh;  // xyz used
+  float ts, iw, lw;   // ts; 1 / |d|; |d|
 };
+
+// the ONB (b1, b2) of a unit direction (Duff et al.)
+__device__ __forceinline__ void onb(const float4 wh, float4& b1, float4& b2) {
+  const float sign = copysignf(1.0f, wh.z);
+  const float a = -frcp(sign + wh.z);  // (1 ulp; the basis only needs orthonormality to ~1e-7)
+  const float b = wh.x * wh.y * a;
+  b1 = make_float4(fmaf(sign * wh.x * wh.x, a, 1.0f), sign * b, -sign * wh.x, 0.0f);
+  b2 = make_float4(b, fmaf(wh.y * wh.y, a, sign), -wh.y, 0.0f);
+}
 
 __device__ __forceinline__ bool frame32(const float4 ray0, const float4 ray1, const float4 P0,
                                         const float4 P3, Setup32& S, float4& rho, float4& c) {
   const float4 w = ray1;
   float ww = fmaf(w.x, w.x, fmaf(w.y, w.y, w.z * w.z));
   bool ok = isfinite(ray0.x) && isfinite(ray0.y) && isfinite(ray0.z) && isfinite(w.x) &&
-            isfinite(w.y) && isfinite(w.z) && !(ray0.w <= 0.0f) && !isnan(ray0.w) && ww > 0.0f;
-  float sign = copysignf(1.0f, w.z);
-  float a = -frcp(sign + w.z);  // (1 ulp; the basis only needs orthonormality to ~1e-7)
-  float b = w.x * w.y * a;
-  S.b1 = make_float4(fmaf(sign * w.x * w.x, a, 1.0f), sign * b, -sign * w.x, 0.0f);
-  S.b2 = make_float4(b, fmaf(w.y * w.y, a, sign), -w.y, 0.0f);
+            isfinite(w.y) && isfinite(w.z) && !(ray0.w <= 0.0f) && !isnan(ray0.w) && ww > 0.0f &&
+            ww < INFINITY;
+  S.iw = frsqrt(ww);
+  S.lw = ww * S.iw;
+  S.wh = make_float4(w.x * S.iw, w.y * S.iw, w.z * S.iw, 0.0f);
+  onb(S.wh, S.b1, S.b2);
   c = make_float4(0.5f * (P0.x + P3.x), 0.5f * (P0.y + P3.y), 0.5f * (P0.z + P3.z), 0.0f);
-  S.iww = frcp(ww);
-  S.ts = fmaf(c.x - ray0.x, w.x, fmaf(c.y - ray0.y, w.y, (c.z - ray0.z) * w.z)) * S.iww;
-  // FP64: v = c - o - ts w (exact inputs), rho = (<v,b1>, <v,b2>, <v,w>)
+  S.ts = fmaf(c.x - ray0.x, w.x, fmaf(c.y - ray0.y, w.y, (c.z - ray0.z) * w.z)) * frcp(ww);
+  // FP64: v = c - o - ts d (exact inputs), rho = (<v,b1>, <v,b2>, <v,w^>)
   double ts = S.ts;
   double vx = fma(-ts, (double)w.x, (double)c.x - (double)ray0.x);
   double vy = fma(-ts, (double)w.y, (double)c.y - (double)ray0.y);
   double vz = fma(-ts, (double)w.z, (double)c.z - (double)ray0.z);
   rho = make_float4((float)fma(vx, (double)S.b1.x, fma(vy, (double)S.b1.y, vz * (double)S.b1.z)),
                     (float)fma(vx, (double)S.b2.x, fma(vy, (double)S.b2.y, vz * (double)S.b2.z)),
-                    (float)fma(vx, (double)w.x, fma(vy, (double)w.y, vz * (double)w.z)), 0.0f);
+                    (float)fma(vx, (double)S.wh.x, fma(vy, (double)S.wh.y, vz * (double)S.wh.z)), 0.0f);
   return ok;
 }
 
@@ -357,21 +366,10 @@ struct Params {
   int closest;  // bit 0: bound each pair's t_max by its ray's best hit so far
                 // (fiber_intersect_closest); bit 1: nearest keys carry the segment index
                 // instead of the pair index (fiber_grid_closest)
-  unsigned int* counter;  // slot: [0-1] K2 pair counter (64-bit), [2] K2 blocks done, [4]/[5] list
-                          // appends (re-run / finalise); [0]-[5] are zero at launch and K2's
-                          // last block returns them to zero after copying [4]/[5] to [6]/[7],
-                          // the list lengths K3 reads (so a slot needs no memset between calls)
-#ifdef FIBER_K3_STREAM
-  // K3 streams the lists while K2 drains: an entry is (seq << 32) | pair, stored with release
-  // semantics after the pair's record, so stale pool memory (other seq) reads as not-ready;
-  // K2's last block stores seq in counter[3] after publishing the lengths in [6]/[7]
-  unsigned long long* list_exact;
-  unsigned long long* list_fin;
-  uint32_t seq;  // unique per call (never 0)
-#else
+  unsigned int* counter;  // this call's own counters (zeroed on its stream): [0-1] K2 pair
+                          // counter (64-bit), [4]/[5] list appends = list lengths for K3
   uint32_t* list_exact;   // pairs K2 flagged for the FP64 re-run   [n_pairs]
   uint32_t* list_fin;     // provisional hits for the FP64 finalise [n_pairs]
-#endif
 #ifdef FIBER_TRACE
   uint32_t trace_pair;  // test build only: per-iteration records of one pair
   float4* trace;        // [kTraceCap] x 3 float4
@@ -499,7 +497,7 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2
     write_record(p, i, pr.x, INFINITY, 0.0f, 0u, FIBER_BAD_INPUT | e.badseg);
     return false;
   }
-  const float4 w = ray1;
+  const float4 w = S.wh;
   // differences are rotated directly, so they keep the relative precision of the inputs
   e.h.L0 = rot(S, w, P0 - c) + rho;
   e.h.L0.w = P0.w;
@@ -515,9 +513,8 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2
     e.h.D1 = rot(S, w, P2 - P1);
     e.h.D2 = rot(S, w, P3 - P2);
   }
-  // ray interval [0, tmax) in local z units: z = (t - ts) |w|^2
-  float ww = 1.0f / S.iww;
-  e.lo0 = -S.ts * ww;
+  // ray interval [0, tmax) in local z units: z = (t - ts) |d|
+  e.lo0 = -S.ts * S.lw;
   float tlim = ray0.w;
   if (p.closest & 1) {
     // the ray's t_max as a running bound: the best hit of the
@@ -529,7 +526,7 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2
       tlim = fminf(tlim, fmaf(tb, 1.9073486328125e-06f, tb) + 1e-30f);
     }
   }
-  e.hi0 = (tlim - S.ts) * ww;
+  e.hi0 = (tlim - S.ts) * S.lw;
   Delta cur;  // conversion {p0,p1,p2,p3} -> {p,d,t0,t1} (3.1 P:372-375)
   cur.p = e.h.L0;
   cur.d = e.h.D0 + e.h.D1 + e.h.D2;
@@ -723,17 +720,9 @@ __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
   }
 }
 
-#ifdef FIBER_K3_STREAM
-__device__ __forceinline__ void list_append(unsigned long long* list, uint32_t k, uint32_t i,
-                                            const Params& p) {
-  const unsigned long long e = ((unsigned long long)p.seq << 32) | i;
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(list + k), "l"(e) : "memory");
-}
-#else
 __device__ __forceinline__ void list_append(uint32_t* list, uint32_t k, uint32_t i, const Params&) {
   list[k] = i;
 }
-#endif
 
 __device__ __forceinline__ uint32_t counter_bits(const Lane& L) {
   return (min(L.backtracks, 255u) << 8) | (min(L.tests, 65535u) << 16);
@@ -776,11 +765,11 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
         const uint2 pr = __ldg(&p.pairs[i]);
         const float4 w = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
 #endif
-        const float sign = copysignf(1.0f, w.z);
-        const float a = -frcp(sign + w.z), b = w.x * w.y * a;
-        const float4 b1 = make_float4(fmaf(sign * w.x * w.x, a, 1.0f), sign * b, -sign * w.x, 0.f);
-        const float4 b2 = make_float4(b, fmaf(w.y * w.y, a, sign), -w.y, 0.f);
-        const float t = zs - L.lo0;  // (z - lo0) / |w|^2, |w| = 1 to FP32 rounding
+        const float iw = frsqrt(fmaf(w.x, w.x, fmaf(w.y, w.y, w.z * w.z)));
+        const float4 wh = make_float4(w.x * iw, w.y * iw, w.z * iw, 0.0f);  // as frame32
+        float4 b1, b2;
+        onb(wh, b1, b2);
+        const float t = (zs - L.lo0) * iw;  // (z - lo0) / |d|
         float u, nx, ny, nz;
         if (kind == FIBER_KIND_CAP0 || kind == FIBER_KIND_CAP1) {
           const Hodo h = hs.load();
@@ -810,9 +799,9 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
           nz = zs - fmaf(ul, c.d.z, c.p.z);
         }
         // back to world coordinates
-        const float wx = fmaf(nx, b1.x, fmaf(ny, b2.x, nz * w.x));
-        const float wy = fmaf(nx, b1.y, fmaf(ny, b2.y, nz * w.y));
-        const float wz = fmaf(nx, b1.z, fmaf(ny, b2.z, nz * w.z));
+        const float wx = fmaf(nx, b1.x, fmaf(ny, b2.x, nz * wh.x));
+        const float wy = fmaf(nx, b1.y, fmaf(ny, b2.y, nz * wh.y));
+        const float wz = fmaf(nx, b1.z, fmaf(ny, b2.z, nz * wh.z));
         write_record(p, i, pr.x, t, u, encode_oct_f(wx, wy, wz),
                      FIBER_HIT | (kind << FIBER_KIND_SHIFT) | counter_bits(L) | badseg);
         return;
@@ -845,7 +834,7 @@ __device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
   Setup32 S;
   float4 rho, c;
   frame32(ray0, ray1, P0, P3, S, rho, c);
-  float t32 = fmaf(rec.x, S.iww, S.ts);
+  float t32 = fmaf(rec.x, S.iw, S.ts);
   float t, u;
   uint32_t n_oct;
   bool hit;
@@ -941,10 +930,6 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base + k >= p.n_pairs) {
         drained = true;
-#ifdef FIBER_K3_STREAM
-        // every pair is claimed: K3 may become resident as K2 blocks exit and stream the lists
-        asm volatile("griddepcontrol.launch_dependents;");
-#endif
       }
       if (!active) {
         const uint32_t i = base + r;
@@ -964,11 +949,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
       if (drained) break;
       continue;
     }
-#ifdef FIBER_UNROLL_EPOCH
-#pragma unroll
-#else
 #pragma unroll 1
-#endif
     for (int k = 0; k < kEpoch; ++k) {
       if (active) {
 #ifdef FIBER_TRACE
@@ -989,23 +970,6 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
   // this warp has no pairs left: K3 (a programmatic dependent) may be scheduled once every
   // block got here; it still waits for K2's completion before reading anything
   asm volatile("griddepcontrol.launch_dependents;");
-  // the last block publishes the list lengths for K3 in slot words 6-7 (stable until the
-  // slot's next use) and returns the slot's working words to zero
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&p.counter[2], 1u) == gridDim.x - 1u) {
-      __threadfence();
-      p.counter[6] = atomicExch(&p.counter[4], 0u);
-      p.counter[7] = atomicExch(&p.counter[5], 0u);
-      atomicExch(pair_counter, 0ull);
-      atomicExch(&p.counter[2], 0u);
-#ifdef FIBER_K3_STREAM
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&p.counter[3]), "r"(p.seq) : "memory");
-#endif
-    }
-  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -1053,82 +1017,15 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   // warp with no divergence; a re-run that hits is finalised by the same lane.  No atomics:
   // both lists are dealt statically from the lengths K2's last block published.
   const uint32_t lane = threadIdx.x & 31u;
-#ifdef FIBER_K3_STREAM
-  // no griddepcontrol.wait: K3 starts while K2 drains and takes each list entry once it is
-  // published (tagged with this call's seq); an index is past the end once K2's last block
-  // has stored seq in counter[3] and the published length says so
-  const uint32_t W = gridDim.x * (blockDim.x >> 5);
-  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint32_t seq = p.seq;
-  // 1 = item in *item, 0 = past the end, -1 = not known yet
-  auto probe = [&](const unsigned long long* list, uint32_t k, int len_word, uint32_t* item) -> int {
-    if (k >= p.n_pairs) return 0;
-    const unsigned long long e = *(const volatile unsigned long long*)(list + k);
-    if ((uint32_t)(e >> 32) == seq) {
-      *item = (uint32_t)e;
-      return 1;
-    }
-    if (*(const volatile uint32_t*)&p.counter[3] == seq) {
-      __threadfence();
-      if (k >= *(const volatile uint32_t*)&p.counter[len_word]) return 0;
-      const unsigned long long e2 = *(const volatile unsigned long long*)(list + k);
-      if ((uint32_t)(e2 >> 32) == seq) {
-        *item = (uint32_t)e2;
-        return 1;
-      }
-    }
-    return -1;
-  };
-  // the whole warp waits until every lane knows its entry, then runs converged
-  auto take = [&](const unsigned long long* list, uint32_t k, int len_word, uint32_t* item) -> int {
-    int r = probe(list, k, len_word, item);
-    while (__any_sync(0xffffffffu, r < 0)) {
-      if (r < 0) {
-        __nanosleep(256);
-        r = probe(list, k, len_word, item);
-      }
-    }
-    __threadfence();  // acquire: the records behind the entries are visible
-    return r;
-  };
-#ifndef FIBER_NO_EXACT
-  for (uint32_t k0 = gw;; k0 += W * 32u) {
-    uint32_t i = 0;
-    const int r = take(p.list_exact, k0 + W * lane, 6, &i);
-    if (r == 1) {
-      exact_one(p, i);
-      if (__float_as_uint(p.hits[i].w) & kProvisional) finalize_one(p, i);
-    }
-    if (__all_sync(0xffffffffu, r == 0)) break;
-  }
-#endif
-#ifndef FIBER_NO_FIN
-  for (uint32_t c = W - 1u - gw;; c += W) {
-    uint32_t i = 0;
-    const int r = take(p.list_fin, c * 32u + lane, 7, &i);
-    if (r == 1) finalize_one(p, i);
-    if (__all_sync(0xffffffffu, r == 0)) break;
-  }
-#endif
-}
-#else
   // launched as a programmatic dependent of K2 (launch_intersect): wait until K2 has
   // completed and its memory (records, lists, list lengths) is visible
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t n_exact = p.counter[6];
-  const uint32_t n_fin = p.counter[7];
+  const uint32_t n_exact = p.counter[4];
+  const uint32_t n_fin = p.counter[5];
   const uint32_t W = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
 #ifndef FIBER_NO_EXACT
-#ifdef FIBER_K3_PACKED  // diagnostic: 32 consecutive re-runs per warp
-  for (uint32_t k = gw * 32u + lane; k < n_exact; k += W * 32u) {
-#else
-#ifndef FIBER_K3_DEAL  // >0: deal the re-runs over only enough warps for ~this many per warp
-#define FIBER_K3_DEAL 0
-#endif
-  const uint32_t We = FIBER_K3_DEAL > 0 ? max(1u, min(W, (n_exact + FIBER_K3_DEAL - 1u) / FIBER_K3_DEAL)) : W;
-  for (uint32_t k = gw + We * lane; gw < We && k < n_exact; k += We * 32u) {
-#endif
+  for (uint32_t k = gw + W * lane; k < n_exact; k += W * 32u) {
     const uint32_t i = p.list_exact[k];
     exact_one(p, i);  // the FP64 traversal, then the finalisation if it hit
     if (__float_as_uint(p.hits[i].w) & kProvisional) finalize_one(p, i);
@@ -1141,7 +1038,6 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
     if (c * 32u + lane < n_fin) finalize_one(p, p.list_fin[c * 32u + lane]);
 #endif
 }
-#endif  // FIBER_K3_STREAM
 
 __global__ void fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1157,11 +1053,8 @@ using namespace fiberx;
 // a call otherwise spends far longer in these queries than the GPU spends on 1M pairs).
 struct LaunchInfo {
   int sms, k2_per_sm, k3_per_sm;
-  unsigned int* slots;  // kSlots x 4 work counters, zero between uses
 };
-constexpr int kSlots = 1024;  // calls in flight on one device at a time (any streams)
-constexpr int kSlotWords = 8;
-static std::atomic<unsigned> g_next_slot{0};
+constexpr size_t kCounterBytes = 256;  // per-call work counters at the head of the scratch
 
 static const LaunchInfo* launch_info() {
   static std::mutex mu;
@@ -1181,9 +1074,6 @@ static const LaunchInfo* launch_info() {
 
     if (li.k2_per_sm < 1) li.k2_per_sm = 1;
     if (li.k3_per_sm < 1) li.k3_per_sm = 1;
-    if (cudaMalloc((void**)&li.slots, kSlots * kSlotWords * sizeof(unsigned int)) != cudaSuccess) return nullptr;
-    if (cudaMemset(li.slots, 0, kSlots * kSlotWords * sizeof(unsigned int)) != cudaSuccess) return nullptr;
-    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
     if (cudaGetLastError() != cudaSuccess || li.sms < 1) return nullptr;
     info[dev] = li;
     ready[dev] = true;
@@ -1235,15 +1125,10 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   int dev = 0;
   cudaGetDevice(&dev);
   cudaMemPool_t pool = scratch_pool(dev);
-  // work counters: a self-resetting slot of the per-device pool
-  const unsigned call_no = g_next_slot.fetch_add(1u);
-  unsigned int* counter = li->slots + kSlotWords * (call_no % kSlots);
-  // the lists first, the records (16-B float4 stores) at the next 256-B boundary
-#ifdef FIBER_K3_STREAM
-  const size_t list_bytes = (2 * (size_t)n_pairs * sizeof(unsigned long long) + 255) & ~(size_t)255;
-#else
-  const size_t list_bytes = (2 * (size_t)n_pairs * sizeof(uint32_t) + 255) & ~(size_t)255;
-#endif
+  // the call's counters, the lists, the records (16-B float4 stores) at 256-B boundaries;
+  // every call owns its counters, so any number of calls may be in flight on any streams
+  const size_t list_bytes =
+      kCounterBytes + ((2 * (size_t)n_pairs * sizeof(uint32_t) + 255) & ~(size_t)255);
   const size_t rec_bytes = hits ? 0 : (size_t)n_pairs * sizeof(fiber_hit);
   void* scratch = nullptr;
   cudaError_t e = pool ? cudaMallocFromPoolAsync(&scratch, list_bytes + rec_bytes, pool, st)
@@ -1254,6 +1139,12 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
     return set_error(FIBER_ECUDA, buf);
   }
   if (!hits) hits = (fiber_hit*)((char*)scratch + list_bytes);
+  unsigned int* counter = (unsigned int*)scratch;
+  e = cudaMemsetAsync(counter, 0, 32, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return set_error(FIBER_ECUDA, "fiber_intersect: counter memset failed");
+  }
   Params p;
   p.rays = (const float4*)rays;
   p.n_rays = n_rays;
@@ -1275,18 +1166,8 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   p.nearest = (unsigned long long*)nearest;
   p.closest = closest;
   p.counter = counter;
-#ifdef FIBER_K3_STREAM
-  p.list_exact = (unsigned long long*)scratch;
-  p.list_fin = (unsigned long long*)scratch + n_pairs;
-  // salted per process, so list memory left by another process cannot carry a matching tag
-  static const unsigned salt =
-      ((unsigned)std::chrono::steady_clock::now().time_since_epoch().count() * 2654435761u) ^
-      (unsigned)getpid();
-  p.seq = (salt + call_no) == 0u ? 1u : salt + call_no;
-#else
-  p.list_exact = (uint32_t*)scratch;
-  p.list_fin = (uint32_t*)scratch + n_pairs;
-#endif
+  p.list_exact = (uint32_t*)((char*)scratch + kCounterBytes);
+  p.list_fin = p.list_exact + n_pairs;
   int64_t chunks = (n_pairs + 31) / 32;
   int64_t blocks = (int64_t)li->sms * li->k2_per_sm;
   if (blocks * kWarps > chunks) blocks = (chunks + kWarps - 1) / kWarps;
@@ -1294,10 +1175,7 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   rc = check_launch("fiber_intersect (traverse)");
   if (rc == FIBER_OK && event_after_traverse) cudaEventRecord((cudaEvent_t)event_after_traverse, st);
   if (rc == FIBER_OK) {
-#ifndef FIBER_K3_GRID  // K3 blocks per SM launched (0: as many as fit)
-#define FIBER_K3_GRID 0
-#endif
-    const int64_t fblocks = (int64_t)li->sms * (FIBER_K3_GRID > 0 ? std::min(FIBER_K3_GRID, li->k3_per_sm) : li->k3_per_sm);
+    const int64_t fblocks = (int64_t)li->sms * li->k3_per_sm;
     // Programmatic dependent launch: K3's launch is processed while K2 drains, and K3 waits
     // for K2's completion on the device (griddepcontrol.wait) -- not with an event in between
     cudaLaunchConfig_t cfg = {};

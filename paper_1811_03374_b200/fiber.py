@@ -6,6 +6,7 @@ a B200 is missing, every call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -113,6 +114,35 @@ def _stream(stream) -> int:
     return stream.cuda_stream
 
 
+def _on(stream):
+    """Run the call's torch work (temporaries, conversions, fills, host reads) on `stream`, the
+    stream its kernels are enqueued on: the caching allocator then orders every temporary's
+    reuse after those kernels, and a host read waits for them."""
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
+def _hits(hits, n: int, device, name="hits"):
+    """A caller-supplied record buffer must hold n float32 [4] records on `device`."""
+    if hits is None:
+        return None
+    if not (isinstance(hits, torch.Tensor) and hits.is_cuda and hits.device == device):
+        raise FiberError(f"{name} must be a CUDA tensor on {device}")
+    if hits.dtype != torch.float32 or hits.dim() != 2 or hits.shape[1] != 4 or hits.shape[0] < n:
+        raise FiberError(f"{name} must be float32 [n_pairs >= {n}, 4], got {hits.dtype} "
+                         f"{tuple(hits.shape)}")
+    if not hits.is_contiguous():
+        raise FiberError(f"{name} must be contiguous")
+    return hits
+
+
+def _nearest(nearest, n_rays: int, device):
+    if not (isinstance(nearest, torch.Tensor) and nearest.is_cuda and nearest.device == device):
+        raise FiberError(f"nearest must be a CUDA tensor on {device}")
+    if nearest.dtype != torch.int64 or tuple(nearest.shape) != (n_rays,) or not nearest.is_contiguous():
+        raise FiberError("nearest must be a contiguous int64[n_rays]")
+    return nearest
+
+
 def _dev(t: torch.Tensor, dtype, shape_tail, name):
     if not (isinstance(t, torch.Tensor) and t.is_cuda):
         raise FiberError(f"{name} must be a CUDA tensor")
@@ -148,6 +178,11 @@ class Segments:
 
 def build_segments(ctrl: torch.Tensor, radii: torch.Tensor, stream=None) -> Segments:
     """fiber_build_segments: ctrl f32[n,4,3], radii f32[n,4] (CUDA) -> Segments."""
+    with _on(stream):
+        return _build_segments(ctrl, radii, stream)
+
+
+def _build_segments(ctrl, radii, stream):
     ctrl = _dev(ctrl, torch.float32, (4, 3), "ctrl")
     radii = _dev(radii, torch.float32, (4,), "radii")
     if radii.shape[0] != ctrl.shape[0]:
@@ -163,6 +198,11 @@ def build_segments(ctrl: torch.Tensor, radii: torch.Tensor, stream=None) -> Segm
 def build_segments_quadratic(ctrl: torch.Tensor, radii: torch.Tensor, stream=None) -> Segments:
     """fiber_build_segments_quadratic: ctrl f32[n,3,3], radii f32[n,3] (CUDA) -> Segments
     (quadratic Bezier segments, degree-elevated exactly by the kernels)."""
+    with _on(stream):
+        return _build_segments_quadratic(ctrl, radii, stream)
+
+
+def _build_segments_quadratic(ctrl, radii, stream):
     ctrl = _dev(ctrl, torch.float32, (3, 3), "ctrl")
     radii = _dev(radii, torch.float32, (3,), "radii")
     if radii.shape[0] != ctrl.shape[0]:
@@ -181,6 +221,11 @@ def presplit(ctrl: torch.Tensor, radii: torch.Tensor, max_level: int = 8,
     f32[n,4], CUDA) until its pieces pass the constraints and the thick-fiber test.  Returns
     dict(ctrl f32[m,4,3], radii f32[m,4], src i32[m], u f32[m,2], valid bool[m],
     offsets i32[n+1]) on the device (one host sync to size the outputs)."""
+    with _on(stream):  # the zero fill, the count kernel and the size read are stream-ordered
+        return _presplit(ctrl, radii, max_level, parametric, stream)
+
+
+def _presplit(ctrl, radii, max_level, parametric, stream):
     ctrl = _dev(ctrl, torch.float32, (4, 3), "ctrl")
     radii = _dev(radii, torch.float32, (4,), "radii")
     n = ctrl.shape[0]
@@ -208,11 +253,13 @@ def presplit(ctrl: torch.Tensor, radii: torch.Tensor, max_level: int = 8,
 def remap_u(hits: torch.Tensor, pairs: torch.Tensor, piece_u: torch.Tensor,
             stream=None) -> torch.Tensor:
     """fiber_remap_u: hit u on a pre-split piece -> u on its source segment (in place)."""
-    pairs = _pairs(pairs)
-    piece_u = _dev(piece_u, torch.float32, (2,), "piece_u")
-    _check(lib().fiber_remap_u(hits.data_ptr(), pairs.data_ptr(), pairs.shape[0],
-                               piece_u.data_ptr(), piece_u.shape[0], _stream(stream)),
-           "fiber_remap_u")
+    with _on(stream):
+        pairs = _pairs(pairs)
+        piece_u = _dev(piece_u, torch.float32, (2,), "piece_u")
+        _hits(hits, pairs.shape[0], pairs.device)
+        _check(lib().fiber_remap_u(hits.data_ptr(), pairs.data_ptr(), pairs.shape[0],
+                                   piece_u.data_ptr(), piece_u.shape[0], _stream(stream)),
+               "fiber_remap_u")
     return hits
 
 
@@ -239,53 +286,66 @@ class Grid:
 
     def candidates(self, rays: torch.Tensor, order: str = "rounds", stream=None):
         """-> (pairs i32[m, 2], offsets i32[n_rays + 1] of the ray-major counts)."""
-        rays = _dev(rays, torch.float32, (8,), "rays")
-        n = rays.shape[0]
-        off = torch.empty(n + 1, dtype=torch.int32, device=rays.device)
-        mx = ctypes.c_uint32()
-        tot = ctypes.c_uint64()
-        _check(lib().fiber_grid_count(self._h, rays.data_ptr(), n, off.data_ptr(),
-                                      ctypes.byref(mx), ctypes.byref(tot), _stream(stream)),
-               "fiber_grid_count")
-        pairs = torch.empty((max(int(tot.value), 1), 2), dtype=torch.int32, device=rays.device)
-        _check(lib().fiber_grid_candidates(self._h, rays.data_ptr(), n, off.data_ptr(), mx.value,
-                                           {"ray": 0, "rounds": 1}[order], pairs.data_ptr(),
-                                           _stream(stream)), "fiber_grid_candidates")
-        return pairs[:int(tot.value)], off
+        with _on(stream):
+            rays = _dev(rays, torch.float32, (8,), "rays")
+            n = rays.shape[0]
+            off = torch.empty(n + 1, dtype=torch.int32, device=rays.device)
+            mx = ctypes.c_uint32()
+            tot = ctypes.c_uint64()
+            _check(lib().fiber_grid_count(self._h, rays.data_ptr(), n, off.data_ptr(),
+                                          ctypes.byref(mx), ctypes.byref(tot), _stream(stream)),
+                   "fiber_grid_count")
+            pairs = torch.empty((max(int(tot.value), 1), 2), dtype=torch.int32, device=rays.device)
+            _check(lib().fiber_grid_candidates(self._h, rays.data_ptr(), n, off.data_ptr(), mx.value,
+                                               {"ray": 0, "rounds": 1}[order], pairs.data_ptr(),
+                                               _stream(stream)), "fiber_grid_candidates")
+            return pairs[:int(tot.value)], off
 
     def closest(self, rays: torch.Tensor, depth: int, nearest: torch.Tensor | None = None,
                 stream=None):
         """fiber_grid_closest: per-ray nearest hit over the grid's candidates with early
         termination -> (keys int64[n_rays] = (bits(t) << 32) | segment, -1 = none; rounds)."""
-        rays = _dev(rays, torch.float32, (8,), "rays")
-        if nearest is None:
-            nearest = torch.empty(rays.shape[0], dtype=torch.int64, device=rays.device)
-        nearest_init(nearest, stream)
-        rounds = ctypes.c_int()
-        _check(lib().fiber_grid_closest(self._h, rays.data_ptr(), rays.shape[0],
-                                        ctypes.byref(self._segs.desc), int(depth),
-                                        nearest.data_ptr(), ctypes.byref(rounds),
-                                        _stream(stream)), "fiber_grid_closest")
-        return nearest, rounds.value
+        with _on(stream):
+            rays = _dev(rays, torch.float32, (8,), "rays")
+            if nearest is None:
+                nearest = torch.empty(rays.shape[0], dtype=torch.int64, device=rays.device)
+            nearest_init(nearest, stream)
+            rounds = ctypes.c_int()
+            _check(lib().fiber_grid_closest(self._h, rays.data_ptr(), rays.shape[0],
+                                            ctypes.byref(self._segs.desc), int(depth),
+                                            nearest.data_ptr(), ctypes.byref(rounds),
+                                            _stream(stream)), "fiber_grid_closest")
+            return nearest, rounds.value
 
 
 def _pairs(pairs: torch.Tensor) -> torch.Tensor:
+    if not (isinstance(pairs, torch.Tensor) and pairs.is_cuda):
+        raise FiberError("pairs must be a CUDA tensor")
     if pairs.dtype in (torch.int64, torch.uint32):
         pairs = pairs.to(torch.int32)
     return _dev(pairs, torch.int32, (2,), "pairs")
+
+
+def _args(rays, pairs):
+    rays = _dev(rays, torch.float32, (8,), "rays")
+    pairs = _pairs(pairs)
+    if pairs.device != rays.device:
+        raise FiberError("rays and pairs must be on the same device")
+    return rays, pairs
 
 
 def intersect(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: int,
               hits: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """fiber_intersect: rays f32[n_rays,8], pairs i32[n_pairs,2] (CUDA) -> hits f32[n_pairs,4]
     (t, u, n_oct bits, flags bits); see unpack()."""
-    rays = _dev(rays, torch.float32, (8,), "rays")
-    pairs = _pairs(pairs)
-    if hits is None:
-        hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=rays.device)
-    _check(lib().fiber_intersect(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
-                                 pairs.data_ptr(), pairs.shape[0], int(depth), hits.data_ptr(),
-                                 _stream(stream)), "fiber_intersect")
+    with _on(stream):
+        rays, pairs = _args(rays, pairs)
+        if hits is None:
+            hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=rays.device)
+        _hits(hits, pairs.shape[0], rays.device)
+        _check(lib().fiber_intersect(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                     pairs.data_ptr(), pairs.shape[0], int(depth),
+                                     hits.data_ptr(), _stream(stream)), "fiber_intersect")
     return hits
 
 
@@ -295,19 +355,22 @@ def intersect_ex(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth:
     """fiber_intersect_ex: intersect (and/or the nearest epilogue); records
     `event_after_traverse` (a torch.cuda.Event) between the traversal and finalisation
     kernels."""
-    rays = _dev(rays, torch.float32, (8,), "rays")
-    pairs = _pairs(pairs)
-    if hits is None and nearest is None:
-        hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=rays.device)
-    ev = None
-    if event_after_traverse is not None:
-        event_after_traverse.record(torch.cuda.current_stream() if stream is None else stream)
-        ev = event_after_traverse.cuda_event
-    _check(lib().fiber_intersect_ex(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
-                                    pairs.data_ptr(), pairs.shape[0], int(depth),
-                                    hits.data_ptr() if hits is not None else None,
-                                    nearest.data_ptr() if nearest is not None else None, ev,
-                                    _stream(stream)), "fiber_intersect_ex")
+    with _on(stream):
+        rays, pairs = _args(rays, pairs)
+        if hits is None and nearest is None:
+            hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=rays.device)
+        _hits(hits, pairs.shape[0], rays.device)
+        if nearest is not None:
+            _nearest(nearest, rays.shape[0], rays.device)
+        ev = None
+        if event_after_traverse is not None:
+            event_after_traverse.record(torch.cuda.current_stream())
+            ev = event_after_traverse.cuda_event
+        _check(lib().fiber_intersect_ex(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                        pairs.data_ptr(), pairs.shape[0], int(depth),
+                                        hits.data_ptr() if hits is not None else None,
+                                        nearest.data_ptr() if nearest is not None else None, ev,
+                                        _stream(stream)), "fiber_intersect_ex")
     return hits
 
 
@@ -315,15 +378,16 @@ def intersect_nearest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, d
                       nearest: torch.Tensor, hits: torch.Tensor | None = None,
                       stream=None) -> torch.Tensor:
     """fiber_intersect_nearest: also atomically keeps, per ray, min((t bits << 32) | pair)."""
-    rays = _dev(rays, torch.float32, (8,), "rays")
-    pairs = _pairs(pairs)
-    if nearest.dtype != torch.int64 or nearest.shape != (rays.shape[0],):
-        raise FiberError("nearest must be int64[n_rays]")
-    _check(lib().fiber_intersect_nearest(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
-                                         pairs.data_ptr(), pairs.shape[0], int(depth),
-                                         hits.data_ptr() if hits is not None else None,
-                                         nearest.data_ptr(), _stream(stream)),
-           "fiber_intersect_nearest")
+    with _on(stream):
+        rays, pairs = _args(rays, pairs)
+        _nearest(nearest, rays.shape[0], rays.device)
+        _hits(hits, pairs.shape[0], rays.device)
+        _check(lib().fiber_intersect_nearest(rays.data_ptr(), rays.shape[0],
+                                             ctypes.byref(segs.desc), pairs.data_ptr(),
+                                             pairs.shape[0], int(depth),
+                                             hits.data_ptr() if hits is not None else None,
+                                             nearest.data_ptr(), _stream(stream)),
+               "fiber_intersect_nearest")
     return nearest
 
 
@@ -332,15 +396,16 @@ def intersect_closest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, d
                       stream=None) -> torch.Tensor:
     """fiber_intersect_closest: intersect_nearest with each pair bounded by its ray's best hit
     so far (order the pairs in candidate rounds, nearest first, for the pruning to bite)."""
-    rays = _dev(rays, torch.float32, (8,), "rays")
-    pairs = _pairs(pairs)
-    if nearest.dtype != torch.int64 or nearest.shape != (rays.shape[0],):
-        raise FiberError("nearest must be int64[n_rays]")
-    _check(lib().fiber_intersect_closest(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
-                                         pairs.data_ptr(), pairs.shape[0], int(depth),
-                                         hits.data_ptr() if hits is not None else None,
-                                         nearest.data_ptr(), _stream(stream)),
-           "fiber_intersect_closest")
+    with _on(stream):
+        rays, pairs = _args(rays, pairs)
+        _nearest(nearest, rays.shape[0], rays.device)
+        _hits(hits, pairs.shape[0], rays.device)
+        _check(lib().fiber_intersect_closest(rays.data_ptr(), rays.shape[0],
+                                             ctypes.byref(segs.desc), pairs.data_ptr(),
+                                             pairs.shape[0], int(depth),
+                                             hits.data_ptr() if hits is not None else None,
+                                             nearest.data_ptr(), _stream(stream)),
+               "fiber_intersect_closest")
     return nearest
 
 
@@ -349,23 +414,32 @@ def compact_hits(hits: torch.Tensor, out: torch.Tensor | None = None,
                  with_idx: bool = True, stream=None):
     """fiber_compact_hits: (out f32[n,4], idx i32[n] or None, count i32[1]) on the device;
     out[:count] are the records with FIBER_HIT in pair order, idx[:count] their pair indices."""
-    hits = _dev(hits, torch.float32, (4,), "hits")
-    n = hits.shape[0]
-    if out is None:
-        out = torch.empty((n, 4), dtype=torch.float32, device=hits.device)
-    if idx is None and with_idx:
-        idx = torch.empty((n,), dtype=torch.int32, device=hits.device)
-    if count is None:
-        count = torch.empty((1,), dtype=torch.int32, device=hits.device)
-    if out.shape[0] < n or (idx is not None and idx.numel() < n):
-        raise FiberError("compact_hits: out / idx must hold n records")
-    _check(lib().fiber_compact_hits(hits.data_ptr(), n, out.data_ptr(),
-                                    idx.data_ptr() if idx is not None else None,
-                                    count.data_ptr(), _stream(stream)), "fiber_compact_hits")
+    with _on(stream):
+        hits = _dev(hits, torch.float32, (4,), "hits")
+        n = hits.shape[0]
+        if out is None:
+            out = torch.empty((n, 4), dtype=torch.float32, device=hits.device)
+        if idx is None and with_idx:
+            idx = torch.empty((n,), dtype=torch.int32, device=hits.device)
+        if count is None:
+            count = torch.empty((1,), dtype=torch.int32, device=hits.device)
+        _hits(out, n, hits.device, "out")
+        if idx is not None and (idx.dtype != torch.int32 or idx.numel() < n or not idx.is_contiguous()
+                                or idx.device != hits.device):
+            raise FiberError("compact_hits: idx must be a contiguous int32[>= n] on the hits' device")
+        if count.dtype != torch.int32 or count.numel() < 1 or count.device != hits.device:
+            raise FiberError("compact_hits: count must be int32[1] on the hits' device")
+        _check(lib().fiber_compact_hits(hits.data_ptr(), n, out.data_ptr(),
+                                        idx.data_ptr() if idx is not None else None,
+                                        count.data_ptr(), _stream(stream)), "fiber_compact_hits")
     return out, idx, count
 
 
 def nearest_init(nearest: torch.Tensor, stream=None) -> torch.Tensor:
+    """fiber_nearest_init: every key to 'no hit' (all ones = -1 as int64)."""
+    if not (isinstance(nearest, torch.Tensor) and nearest.is_cuda and nearest.dtype == torch.int64
+            and nearest.is_contiguous()):
+        raise FiberError("nearest must be a contiguous CUDA int64 tensor")
     _check(lib().fiber_nearest_init(nearest.data_ptr(), nearest.numel(), _stream(stream)),
            "fiber_nearest_init")
     return nearest

@@ -62,8 +62,24 @@ def compare(g: dict, o: dict) -> dict:
     }
 
 
-def assert_parity(rep: dict, max_excluded_frac: float = 0.05):
+def oracle_exclusions(o: dict) -> int:
+    """Pairs the comparison leaves out, decided by the oracle alone: grazing (hit flag differs
+    between its +eps and -eps runs), or hits whose value is ill-conditioned at the eps scale."""
+    p, m = o["plus"], o["minus"]
+    with np.errstate(invalid="ignore"):
+        stable = (~o["kind_unstable"]) & (p["kind"] == m["kind"])
+        stable &= np.abs(p["t"] - m["t"]) <= TOL_T * np.abs(o["t"])
+        stable &= np.abs(p["u"] - m["u"]) <= TOL_U
+        stable &= _angle(p["n"], m["n"]) <= TOL_N
+    return int((o["grazing"] | (o["hit"] & ~stable)).sum())
+
+
+def assert_parity(rep: dict, max_excluded_frac: float | None = 0.0):
+    """Hit flags and values as the bar above; exclusions (grazing pairs + hits with
+    ill-conditioned values) at most max_excluded_frac of the hits (None: not bounded, for sets
+    built inside the band).  The default 0 is the level every C1-C3, C5, glancing and edge
+    set measures (R5); C3 at D=16 and C4 pass their measured level plus a margin."""
     assert rep["hit_mismatch"] == 0, rep
     assert rep["value_mismatch"] == 0, rep
-    if rep["hits"] > 100:
+    if max_excluded_frac is not None:
         assert rep["excluded_values"] + rep["grazing"] <= max_excluded_frac * max(rep["hits"], 1), rep

@@ -122,3 +122,58 @@ def test_argument_errors_raise(fx):
     empty = fx.intersect(rays, segs, pairs[:0], 4)
     assert empty.shape == (0, 4)
     torch.cuda.synchronize()
+
+
+def test_many_calls_in_flight_on_several_streams(fx):
+    """Every call owns its work counters: 2,048 calls queued on 4 streams without a
+    host sync in between give the records of one call each."""
+    import torch
+
+    w = gen.config2("A", n_rays=1 << 10, depth=16)
+    rays, segs, pairs = fx.to_device(w)
+    ref = fx.intersect(rays, segs, pairs, 16)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [torch.empty_like(ref) for _ in range(2048)]
+    for k, o in enumerate(outs):
+        s = streams[k % 4]
+        s.wait_stream(torch.cuda.current_stream())
+        fx.intersect(rays, segs, pairs, 16, hits=o, stream=s)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.view(torch.int32), ref.view(torch.int32))
+
+
+def test_argument_validation_of_buffers(fx):
+    import torch
+
+    w = gen.config2("A", n_rays=256, depth=4)
+    rays, segs, pairs = fx.to_device(w)
+    for bad in (torch.empty((255, 4), device="cuda"), torch.empty((256, 4), dtype=torch.float64,
+                                                                  device="cuda"),
+                torch.empty((256, 8), device="cuda")[:, :4], torch.empty((256, 4))):
+        with pytest.raises(fx.FiberError):
+            fx.intersect(rays, segs, pairs, 4, hits=bad)
+    with pytest.raises(fx.FiberError):
+        fx.intersect_nearest(rays, segs, pairs, 4, torch.empty(256, dtype=torch.int32, device="cuda"))
+    with pytest.raises(fx.FiberError):
+        fx.nearest_init(torch.empty(256, dtype=torch.int32, device="cuda"))
+
+
+def test_explicit_stream_temporaries(fx):
+    """pairs given as int64 (converted to a temporary) on a side stream: the result equals the
+    current-stream call (the temporary lives on the launch stream)."""
+    import torch
+
+    w = gen.config2("C", n_rays=1 << 14, depth=9)
+    rays, segs, pairs = fx.to_device(w)
+    ref = fx.intersect(rays, segs, pairs, 9)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    p64 = pairs.to(torch.int64)
+    out = torch.empty_like(ref)
+    fx.intersect(rays, segs, p64, 9, hits=out, stream=s)
+    junk = [torch.full((1 << 16, 2), -1, dtype=torch.int32, device="cuda") for _ in range(8)]
+    torch.cuda.synchronize()
+    del junk
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))

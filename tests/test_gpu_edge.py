@@ -1,0 +1,113 @@
+"""GPU-vs-oracle parity on the listing-defect edge cases (VERDICT r1 items 2/"next" 1b; SURVEY
+4.2 "one regression per defect"): F3 perpendicular rays and partition planes (P:1442-1449,
+P:1466-1473), F4 axis-parallel rays, F2/F6 cap entries, F5 hits at
+t == t_max, INSIDE origins, the straight cylinder's closed-form set, non-unit
+directions and the grazing band itself, at D in {0, 1, 2, 4, 9, 16, 22, 23}.  Inputs:
+tests/edge_sets.py.  Needs a B200."""
+import numpy as np
+import pytest
+
+import oracle
+from tests import edge_sets as es
+from tests.parity import assert_parity, compare
+from tests.test_oracle_closed_forms import finite_cylinder_hit
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+DEPTHS = [0, 1, 2, 4, 9, 16, 22, 23]
+
+
+@pytest.fixture(scope="module")
+def fx():
+    import torch
+
+    import paper_1811_03374_b200 as fx
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return fx
+
+
+def _both(fx, rays, ctrl, radii, depth):
+    w = gen.Workload("edge", rays, ctrl, radii, gen.make_pairs_1seg(rays.shape[0]), depth)
+    r, s, p = fx.to_device(w)
+    g = fx.unpack(fx.intersect(r, s, p, depth))
+    o = oracle.intersect(rays, ctrl, radii, w.pairs, depth)
+    return g, o, compare(g, o)
+
+
+@pytest.mark.parametrize("axis", [(1, 0, 0), (0, 1, 0), (0, 0, 1)])
+@pytest.mark.parametrize("depth", DEPTHS)
+def test_straight_cylinder_closed_form_set(fx, axis, depth):
+    g, o, rep = _both(fx, *es.straight(axis), depth)
+    assert_parity(rep, max_excluded_frac=0.0)
+    assert rep["hits"] > 150
+    caps = (o["kind"] == 1) | (o["kind"] == 2)
+    assert caps.sum() > 20 and np.array_equal(g["kind"][caps], o["kind"][caps])
+
+
+@pytest.mark.parametrize("depth", DEPTHS)
+def test_F3_perpendicular_rays(fx, depth):
+    rays = es.perpendicular()[0]
+    g, o, rep = _both(fx, *es.perpendicular(), depth)
+    assert_parity(rep, max_excluded_frac=None)  # only the 2 rays exactly on a cap plane:
+    assert rep["grazing"] == es.perpendicular_on_cap(rays).sum() == 2
+    assert rep["excluded_values"] == 0 and rep["hits"] > 100
+    beyond = (rays[:, 0] > 6.0) | (rays[:, 0] < 0.0)
+    assert not g["hit"][beyond].any()  # no false hits beyond the caps (F3)
+
+
+@pytest.mark.parametrize("depth", DEPTHS)
+def test_F4_F2_F6_axial_rays(fx, depth):
+    rays, ctrl, radii = es.axial()
+    g, o, rep = _both(fx, rays, ctrl, radii, depth)
+    assert_parity(rep, max_excluded_frac=0.0)
+    ins = o["kind"] == oracle.KIND_INSIDE
+    assert ins.sum() > 10 and g["inside"][ins].all() and (g["t"][ins] == 0).all()
+    cap = (o["kind"] == 1) | (o["kind"] == 2)
+    assert cap.sum() > 100 and np.array_equal(g["kind"][cap], o["kind"][cap])
+    assert (g["u"][o["kind"] == 1] == 0).all() and (g["u"][o["kind"] == 2] == 1).all()
+
+
+@pytest.mark.parametrize("depth", [0, 2, 9, 22, 23])
+def test_F5_hit_at_tmax(fx, depth):
+    """t_max = fl32(t*), one float above and one below, for the straight cylinder's hits:
+    exactly at t_max is a miss, one ulp above a hit, one below a miss (F5)."""
+    rays, ctrl, radii = es.straight((1, 0, 0), n=400)
+    A, B = ctrl[0, 0].astype(float), ctrl[0, 3].astype(float)
+    t = np.array([(finite_cylinder_hit(ry[:3], ry[4:7], A, B, float(radii[0, 0])) or (np.nan,))[0]
+                  for ry in rays.astype(np.float64)])
+    keep = np.isfinite(t) & (t > 0)
+    r3 = es.tmax_boundary(t[keep], rays[keep])
+    g, o, rep = _both(fx, r3, ctrl, radii, depth)
+    assert_parity(rep, max_excluded_frac=0.0)
+    k = keep.sum()
+    assert o["hit"][k:2 * k].all() and not o["hit"][2 * k:].any()
+
+
+@pytest.mark.parametrize("fiber", ["A", "C"])
+@pytest.mark.parametrize("depth", [1, 4, 9, 16, 22])
+def test_inside_origins(fx, fiber, depth):
+    g, o, rep = _both(fx, *es.inside(fiber), depth)
+    assert_parity(rep, max_excluded_frac=0.0)
+    ins = o["kind"] == oracle.KIND_INSIDE
+    assert ins.sum() > 0.9 * ins.size and g["inside"][ins].all()
+
+
+@pytest.mark.parametrize("fiber", ["A", "C"])
+@pytest.mark.parametrize("depth", [2, 9, 16, 22])
+def test_non_unit_directions(fx, fiber, depth):
+    """Directions scaled by 1/8..8: t is the parameter along d as given (include/fiber.h)."""
+    g, o, rep = _both(fx, *es.scaled(fiber), depth)
+    assert_parity(rep, max_excluded_frac=0.0)
+    assert rep["hits"] > 300
+
+
+@pytest.mark.parametrize("depth", [0, 4, 12, 22])
+def test_grazing_band_set(fx, depth):
+    """Rays at 0..3000 eps from the surface: outside the oracle's band the hit flag is exact
+    (compare() excludes only the oracle's grazing pairs)."""
+    g, o, rep = _both(fx, *es.band(), depth)
+    assert_parity(rep, max_excluded_frac=None)
+    assert 0 < rep["grazing"] < 0.5 * rep["n"]
+    assert rep["hits"] > 100

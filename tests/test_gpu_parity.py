@@ -111,7 +111,7 @@ def test_curved_thick_low_depth_parity(fx, shape, radius, depth):
     w = gen.Workload("curved", gen._pack_rays(orig, tgt - orig), ctrl, radii,
                      gen.make_pairs_1seg(n), depth)
     rep = compare(_run(fx, w), _oracle(w))
-    assert_parity(rep)
+    assert_parity(rep, max_excluded_frac=0.001)  # measured: 1 of 4318 hits (quarter arc, D=6)
     assert rep["hits"] > 2000
 
 
@@ -131,7 +131,9 @@ def test_config3_hair_parity(fx, depth):
     """C3 recipe (hair patch, varying radii, 16 candidates per targeted ray), subsampled."""
     w = _c3(depth)
     rep = compare(_run(fx, w), _oracle(w))
-    assert_parity(rep)
+    # measured: 0 at D=9; 40 of 19,064 hits (0.21%) at D=16 whose value the oracle's own
+    # +-eps runs move by more than the tolerance (near-tangent entries, DESIGN.md R5)
+    assert_parity(rep, max_excluded_frac={9: 0.0, 16: 0.005}[depth])
     assert rep["hits"] > 500
 
 
@@ -140,7 +142,7 @@ def test_config4_thin_grazing_parity(fx, depth):
     """C4 recipe (r = 1e-4 chord, half the rays within +-2e-3 r of the silhouette)."""
     w = _c4(depth)
     rep = compare(_run(fx, w), _oracle(w))
-    assert_parity(rep, max_excluded_frac=0.1)
+    assert_parity(rep, max_excluded_frac=0.002)  # measured <= 11 of 24,590 hits (0.045%)
     assert rep["hits"] > 0.5 * (1 << 14)
 
 
@@ -194,7 +196,7 @@ def test_full_size_config4_sampled(fx):
     8192-pair sample compared with the oracle (grazing-band exclusions as the subsampled
     test)."""
     w = gen.config4()
-    g, o, rep = _sampled(fx, w, 8192, 41, max_excluded_frac=0.1)
+    g, o, rep = _sampled(fx, w, 8192, 41, max_excluded_frac=0.002)  # measured 2 of 6,138
     assert abs(g["hit"].mean() - o["hit"].mean()) < 0.02
 
 
