@@ -621,8 +621,12 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
     // below the crop level the leaf index is only known to about (error of c0 along the
     // axis) / (leaf length) = tau |d_z| / |d|^2 leaves; K3 walks up to kWalk of them, so
     // nearly parallel rays that could be further off are re-run in FP64
+    // An INSIDE entry (the origin bounds t_min) below the crop level is re-run too: the FP32
+    // descent there orders children by the cylinder entry behind the origin and does not crop,
+    // so its leaf can be far from the one holding the origin.
     if (L.size < kCropMinSize)
-      note_tie(L, hs, L.delta * inv_sin * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d) ? 8u : 0u);
+      note_tie(L, hs, (L.delta * inv_sin * fabsf(L.cur.d.z) > (float)kWalk * dot3(L.cur.d, L.cur.d) ||
+                       (L.tag == TAG_ORIGIN && !(c0 >= L.tmin))) ? 8u : 0u);
     L.c0 = c0;
     return ST_HIT;
   }
@@ -830,11 +834,12 @@ __device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
   const bool exact_leaf = (y & kExactLeaf) != 0u;
   const uint32_t lo_tag = __float_as_uint(rec.z);
   uint32_t flags = __float_as_uint(rec.w) & ~kProvisional;
-  // the FP32 z* as a ray parameter (only used for WEDGE / INSIDE entries)
+  // the FP32 z* as a ray parameter (only used for WEDGE entries); an INSIDE entry is the ray
+  // origin itself, t* = 0 (F2 with t_min = 0; a re-run record carries no z*)
   Setup32 S;
   float4 rho, c;
   frame32(ray0, ray1, P0, P3, S, rho, c);
-  float t32 = fmaf(rec.x, S.iw, S.ts);
+  float t32 = inside ? 0.0f : fmaf(rec.x, S.iw, S.ts);
   float t, u;
   uint32_t n_oct;
   bool hit;

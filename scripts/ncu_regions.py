@@ -10,7 +10,7 @@ import sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "-k", "regex:intersect_kernel"], capture_output=True, text=True).stdout
+                      "-k", "regex:" + (sys.argv[3] if len(sys.argv) > 3 else "traverse_kernel")], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 agg, th, st, src = collections.Counter(), collections.Counter(), collections.Counter(), {}
 cur = None
