@@ -324,6 +324,15 @@ __device__ __forceinline__ void onb(const float4 wh, float4& b1, float4& b2) {
   b2 = make_float4(b, fmaf(wh.y * wh.y, a, sign), -wh.y, 0.0f);
 }
 
+// |d|^2 within 2^-22 of 1: unit to FP32 rounding (the SPEC contract S:34; every normalised
+// FP32 vector).  K2 traverses only such rays, in the frame of w^ = d as is;
+// any other d is traversed by K3 in FP64 (exact.cuh normalises it), t along d as given.
+__device__ __forceinline__ bool unit_dir(float ww) {
+  return fabsf(ww - 1.0f) <= 2.384185791015625e-07f;
+}
+
+// kUnit: the caller has checked unit_dir (K2); otherwise d is normalised (K3's finalisation)
+template <bool kUnit>
 __device__ __forceinline__ bool frame32(const float4 ray0, const float4 ray1, const float4 P0,
                                         const float4 P3, Setup32& S, float4& rho, float4& c) {
   const float4 w = ray1;
@@ -331,9 +340,9 @@ __device__ __forceinline__ bool frame32(const float4 ray0, const float4 ray1, co
   bool ok = isfinite(ray0.x) && isfinite(ray0.y) && isfinite(ray0.z) && isfinite(w.x) &&
             isfinite(w.y) && isfinite(w.z) && !(ray0.w <= 0.0f) && !isnan(ray0.w) && ww > 0.0f &&
             ww < INFINITY;
-  S.iw = frsqrt(ww);
-  S.lw = ww * S.iw;
-  S.wh = make_float4(w.x * S.iw, w.y * S.iw, w.z * S.iw, 0.0f);
+  S.iw = kUnit ? 1.0f : frsqrt(ww);
+  S.lw = kUnit ? 1.0f : ww * S.iw;
+  S.wh = kUnit ? w : make_float4(w.x * S.iw, w.y * S.iw, w.z * S.iw, 0.0f);
   onb(S.wh, S.b1, S.b2);
   c = make_float4(0.5f * (P0.x + P3.x), 0.5f * (P0.y + P3.y), 0.5f * (P0.z + P3.z), 0.0f);
   S.ts = fmaf(c.x - ray0.x, w.x, fmaf(c.y - ray0.y, w.y, (c.z - ray0.z) * w.z)) * frcp(ww);
@@ -493,8 +502,15 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2
   e.pair = i;
   Setup32 S;
   float4 rho, c;
-  if (!frame32(ray0, ray1, P0, P3, S, rho, c)) {
+  if (!frame32<true>(ray0, ray1, P0, P3, S, rho, c)) {
     write_record(p, i, pr.x, INFINITY, 0.0f, 0u, FIBER_BAD_INPUT | e.badseg);
+    return false;
+  }
+  if (!unit_dir(fmaf(ray1.x, ray1.x, fmaf(ray1.y, ray1.y, ray1.z * ray1.z)))) {
+    // a non-unit direction: the whole traversal runs in FP64 (K3), from the root
+    p.hits[i] = make_float4(__uint_as_float((uint32_t)FIBER_MAX_DEPTH << 24), 0.0f, 0.0f,
+                            __uint_as_float(e.badseg | kUncertain));
+    p.list_exact[atomicAdd(&p.counter[4], 1u)] = i;
     return false;
   }
   const float4 w = S.wh;
@@ -769,11 +785,10 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
         const uint2 pr = __ldg(&p.pairs[i]);
         const float4 w = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
 #endif
-        const float iw = frsqrt(fmaf(w.x, w.x, fmaf(w.y, w.y, w.z * w.z)));
-        const float4 wh = make_float4(w.x * iw, w.y * iw, w.z * iw, 0.0f);  // as frame32
+        const float4 wh = w;  // a unit direction (prepare), as frame32<true>
         float4 b1, b2;
         onb(wh, b1, b2);
-        const float t = (zs - L.lo0) * iw;  // (z - lo0) / |d|
+        const float t = zs - L.lo0;  // (z - lo0) / |d|, |d| = 1
         float u, nx, ny, nz;
         if (kind == FIBER_KIND_CAP0 || kind == FIBER_KIND_CAP1) {
           const Hodo h = hs.load();
@@ -838,7 +853,7 @@ __device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
   // origin itself, t* = 0 (F2 with t_min = 0; a re-run record carries no z*)
   Setup32 S;
   float4 rho, c;
-  frame32(ray0, ray1, P0, P3, S, rho, c);
+  frame32<false>(ray0, ray1, P0, P3, S, rho, c);
   float t32 = inside ? 0.0f : fmaf(rec.x, S.iw, S.ts);
   float t, u;
   uint32_t n_oct;

@@ -106,10 +106,13 @@ def constraint_margins(P: np.ndarray) -> np.ndarray:
 
 
 def thick_ok(P: np.ndarray, rbar: np.ndarray, samples: int = 256,
-             end_samples: int = 0) -> np.ndarray:
+             end_samples: int = 0, device=None) -> np.ndarray:
     """Sampled stand-in for the thick-fiber test: no point of the normal disc of
     radius rbar at any sampled u reaches beyond the segment's end planes.  end_samples adds
-    samples approaching both ends (u = 2^-j, 1 - 2^-j), where crossings start."""
+    samples approaching both ends (u = 2^-j, 1 - 2^-j), where crossings start.  device: the
+    same formulas in torch float64 on that device (large segment sets, e.g. C5's 2^21)."""
+    if device is not None:
+        return _thick_ok_torch(P, rbar, samples, end_samples, device)
     u = np.linspace(0.0, 1.0, samples)
     if end_samples:
         e = 2.0 ** -np.arange(1, end_samples + 1)
@@ -133,6 +136,38 @@ def thick_ok(P: np.ndarray, rbar: np.ndarray, samples: int = 256,
         sl = slice(1, None) if end == 0 else slice(0, -1)
         ok &= np.all(ext[:, sl] <= 1e-12, axis=1)
     return ok
+
+
+def _thick_ok_torch(P, rbar, samples, end_samples, device):
+    import torch
+
+    u = np.linspace(0.0, 1.0, samples)
+    if end_samples:
+        e = 2.0 ** -np.arange(1, end_samples + 1)
+        u = np.sort(np.r_[u, e, 1.0 - e])
+    ut = torch.from_numpy(u).to(device)[None, :, None]
+    v = 1.0 - ut
+    out = np.empty(P.shape[0], dtype=bool)
+    chunk = max(1, (1 << 26) // len(u))
+    for a in range(0, P.shape[0], chunk):
+        Q = torch.from_numpy(np.ascontiguousarray(P[a:a + chunk, :, :3], dtype=np.float64)).to(device)
+        rb = torch.from_numpy(np.ascontiguousarray(rbar[a:a + chunk], dtype=np.float64)).to(device)
+        p0, p1, p2, p3 = (Q[:, k][:, None, :] for k in range(4))
+        X = v ** 3 * p0 + 3 * ut * v * v * p1 + 3 * ut * ut * v * p2 + ut ** 3 * p3
+        T = 3 * (v * v * (p1 - p0) + 2 * ut * v * (p2 - p1) + ut * ut * (p3 - p2))
+        T = T / torch.linalg.norm(T, dim=-1, keepdim=True)
+        ok = torch.ones(Q.shape[0], dtype=torch.bool, device=device)
+        for end, (i0, i1) in ((0, (0, 1)), (1, (3, 2))):
+            q = Q[:, i0]
+            n = Q[:, i0] - Q[:, i1]
+            n = n / torch.linalg.norm(n, dim=-1, keepdim=True)
+            tn = (T * n[:, None, :]).sum(-1)
+            ext = ((X - q[:, None, :]) * n[:, None, :]).sum(-1) + rb[:, None] * torch.sqrt(
+                torch.clamp(1 - tn * tn, min=0))
+            ext = ext[:, 1:] if end == 0 else ext[:, :-1]
+            ok &= (ext <= 1e-12).all(dim=1)
+        out[a:a + chunk] = ok.cpu().numpy()
+    return out
 
 
 def _pack_rays(orig: np.ndarray, dirs: np.ndarray, tmax=np.inf) -> np.ndarray:
@@ -389,8 +424,9 @@ def hair_patch(seed: int = 3374, n_side: int = 100, n_seg: int = 10, thin: bool 
     return _validate(segs, radii)
 
 
-def fur_ball(seed: int = 3376, n_strands: int = 524288, n_seg: int = 4):
-    """Fur: strands on the unit sphere, length 0.2, outward, curl <= 20 deg per segment."""
+def fur_ball(seed: int = 3376, n_strands: int = 524288, n_seg: int = 4, device=None):
+    """Fur: strands on the unit sphere, length 0.2, outward, curl <= 20 deg per segment.
+    device: run the sampled validity check there (torch float64; see thick_ok)."""
     rng = _rng(seed)
     roots = _sphere(rng, n_strands)
     pts = _random_walk(rng, roots, roots.copy(), n_seg, 0.2 / n_seg, 20.0)
@@ -398,10 +434,10 @@ def fur_ball(seed: int = 3376, n_strands: int = 524288, n_seg: int = 4):
     k = np.tile(np.arange(n_seg), n_strands).astype(np.float64)
     s = (k[:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None]) / n_seg
     radii = 1.5e-3 + (4e-4 - 1.5e-3) * s
-    return _validate(segs, radii)
+    return _validate(segs, radii, device)
 
 
-def _validate(segs: np.ndarray, radii: np.ndarray):
+def _validate(segs: np.ndarray, radii: np.ndarray, device=None):
     """Enforce the preconditions of the path on every segment (SURVEY 8(d) "Inputs"):
     the five constraints, |t0|, |t1| >= 0.05 |d|, and the sampled thick-fiber check.
     A violating segment is straightened towards its chord until valid."""
@@ -414,7 +450,7 @@ def _validate(segs: np.ndarray, radii: np.ndarray):
         t0 = np.linalg.norm(sg[:, 1] - sg[:, 0], axis=1)
         t1 = np.linalg.norm(sg[:, 3] - sg[:, 2], axis=1)
         ok = (m.min(1) >= 1e-3 * d * d) & (t0 >= 0.05 * d) & (t1 >= 0.05 * d)
-        ok &= thick_ok(sg, radii[todo].max(1))
+        ok &= thick_ok(sg, radii[todo].max(1), device=device)
         if ok.all():
             break
         todo = todo[~ok]
@@ -498,29 +534,45 @@ def config4(seed: int = 3375, n_rays: int = 1 << 24, depth: int = 22) -> Workloa
 
 
 def config5(seed: int = 3376, n_rays: int = 1 << 24, k: int = 16, depth: int = 6,
-            n_strands: int = 524288, ray_range: tuple[int, int] | None = None) -> Workload:
+            n_strands: int = 524288, ray_range: tuple[int, int] | None = None,
+            ray_ids: np.ndarray | None = None, device=None) -> Workload:
     """C5: fur, 2^21 segments, 2^24 targeted rays x 16 candidates = 2^28 pairs, D = 6.
-    ray_range=(a, b) generates only the pairs of rays a..b-1 (per-rank shard) -- the rays,
-    segments and candidate choice are identical to the full generation."""
+    ray_range=(a, b) generates only the pairs of rays a..b-1, ray_ids only those of the given
+    rays (a rank's shard, paper_1811_03374_b200.dist) -- the rays, segments and candidate
+    choice are identical to the full generation.  Pairs are sorted by (segment, ray).
+    device: run the validity check and the pair sort there (torch; the bench's full size)."""
     from scipy.spatial import cKDTree
 
-    ctrl, radii = fur_ball(seed, n_strands)
+    ctrl, radii = fur_ball(seed, n_strands, device=device)
     rng = _rng(seed + 1)
     seg = rng.integers(0, ctrl.shape[0], n_rays)
     w = _sphere(rng, n_rays)
     tgt = _targets_on_segments(rng, ctrl, radii, seg, w, -1.5, 0.5)
     orig = tgt - 0.5 * w
     rays = _pack_rays(orig, w)
-    a, b = ray_range if ray_range is not None else (0, n_rays)
+    if ray_ids is None:
+        a, b = ray_range if ray_range is not None else (0, n_rays)
+        ray_ids = np.arange(a, b)
+        name = f"C5:fur2M:rays[{a},{b})"
+    else:
+        ray_ids = np.sort(np.asarray(ray_ids, dtype=np.int64))
+        name = f"C5:fur2M:{ray_ids.size}rays"
     centers = 0.5 * (ctrl.min(1) + ctrl.max(1)).astype(np.float64)
-    _, nn = cKDTree(centers).query(tgt[a:b], k=k, workers=-1)
+    _, nn = cKDTree(centers).query(tgt[ray_ids], k=k, workers=-1)
     nn = np.asarray(nn)
-    has = (nn == seg[a:b, None]).any(1)
-    nn[~has, -1] = seg[a:b][~has]
-    pairs = np.stack([np.repeat(np.arange(a, b), k), nn.ravel()], 1).astype(np.uint32)
-    order = np.lexsort((pairs[:, 0], pairs[:, 1]))
-    return Workload(f"C5:fur2M:rays[{a},{b})", rays, ctrl, radii,
-                    np.ascontiguousarray(pairs[order]), depth, {"seed": seed})
+    has = (nn == seg[ray_ids, None]).any(1)
+    nn[~has, -1] = seg[ray_ids][~has]
+    pairs = np.stack([np.repeat(ray_ids, k), nn.ravel()], 1).astype(np.uint32)
+    # (seg, ray) order: the pairs are ray-major, so a stable sort by segment alone gives it
+    if device is not None:
+        import torch
+
+        key = torch.from_numpy(pairs[:, 1].astype(np.int64)).to(device)
+        order = torch.sort(key, stable=True).indices.cpu().numpy()
+    else:
+        order = np.lexsort((pairs[:, 0], pairs[:, 1]))
+    return Workload(name, rays, ctrl, radii, np.ascontiguousarray(pairs[order]), depth,
+                    {"seed": seed})
 
 
 def straight_fiber(length: float = 6.0, r0: float = 0.1, r3: float | None = None,
