@@ -1,25 +1,45 @@
 #!/usr/bin/env python
 """Benchmark of the ray/fiber hot path (BASELINE.json metric: G ray-fiber tests/s vs
-subdivision depth 2-22, % of the FP32 roofline).
+subdivision depth 2-22 on 1/2/4/8 B200, % of the FP32 roofline).
 
-Workload (N = 1): config C2 -- each of the three single fibers F_A, F_B, F_C against 2^20
+value (every N): config C2 -- each of the three single fibers F_A, F_B, F_C against 2^20
 random rays, at every depth D = 2..22 (Fig. 1).  One step = the whole
-sweep: 3 fibers x 21 depths = 63 launches of fiber_intersect, 66,060,288 ray-segment tests.
-With N > 1 ranks (torchrun), every rank runs the same sweep on its own rays (weak scaling:
-rays are sharded, segments replicated); after the timed region the
-per-ray hit records are gathered with one NCCL all_gather.
+sweep: 3 fibers x 21 depths = 63 launches of fiber_intersect, 66,060,288 ray-segment tests
+per rank.  With N ranks every rank runs the sweep on its own rays: the pairs are independent
+units, sharded with no collective (weak scaling).
 
-Timing: W untimed warm-up steps, then K steps.  Every launch is bracketed by CUDA events on
-its stream and preceded (untimed) by a 256 MiB write that flushes the 126 MB L2, so every
-launch reads its rays/pairs from HBM.  value = all ranks' tests / max over ranks of the
-summed kernel time.  `--impl reference` times the FP64 CPU oracle instead (bounded sample).
+Extra keys of the same JSON line:
+  configs.C3 / configs.C4 (N = 1): BASELINE configs 3 and 4 at full size, device-timed the
+      same way, each with its own roofline and (in the cpu_baseline leg) sampled parity.
+  c5 (every N): BASELINE config 5 -- 2^24 fur rays x 16 candidates = 2^28 pairs at D = 6 in
+      TOTAL, rays shuffled and blocked over the N ranks (strong scaling), each rank's shard in
+      chunk launches of the nearest-hit epilogue with the per-ray records gathered by NCCL
+      all_gather_into_tensor on a second stream, overlapping the next chunk's kernels
+      (paper_1811_03374_b200.dist.ShardedNearest).
+  roofline: the dominant kernel (K2, intersect_kernel) on C2: algorithmic FP32 flops per
+      launch (per-pair counters x per-step flops, table below) / its CUDA-event time; issue,
+      SIMT and DRAM from the committed ncu summary only if it was taken of this very build
+      (sha256 of libfiber.so), else null.
+  e2e: the same sweep through the public API from pinned host buffers (copies timed).
+  cpu_baseline (N = 1, rank 0): the FP64 oracle as it stands on bounded samples of C2 (the
+      timed value), C3, C4 and C5; on the same samples it reports the parity of the GPU's
+      records (the bar of tests/parity.py).
+
+Timing: W untimed warm-up steps, then K steps.  Every C2/C3/C4 launch is bracketed by CUDA
+events on its stream and preceded (untimed) by a 256 MiB write that flushes the 126 MB L2.
+value = all ranks' tests / max over ranks of the summed kernel time.  --gpus N > 1 without a
+torchrun environment re-launches itself under torch.distributed.run with N ranks.
+`--impl reference` times the FP64 CPU oracle instead (bounded sample).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -35,10 +55,16 @@ FIBERS = ("A", "B", "C")
 DEPTHS = tuple(range(2, 23))
 N_RAYS = 1 << 20
 
-# Algorithmic FP32 flops per occurrence of each step of the loop (FMA = 2, MUFU = 1),
-# counted from the kernel source: a3 node test, a4 descend,
-# a5 backtrack (cached-parent path).
-FLOPS_TEST, FLOPS_DESCEND, FLOPS_BACKTRACK = 72, 56, 68
+# Algorithmic flops per occurrence of each step of SURVEY 8(a) (FMA = 2, add/mul = 1,
+# MUFU rcp/sqrt/rsqrt = 1, FP64 ops counted alike; compares, min/max and selects = 0),
+# counted from the kernel source (DESIGN.md section 6 "Roofline" has the itemised table):
+#   a2 setup (frame32 incl. the FP64 origin shift, 4 rotations, root slab, error scale)  189
+#   a3 node test (conservative radius, App. A cylinder, near-tie bounds)                 82
+#   a4 descend (split point/tangent, partition plane, near-tie, child)                   57
+#   a5 backtrack (cached parent: the same split of the parent; re-calculation is rarer)  57
+#   a7 FP32 finalisation of a hit (frame back-rotation, u, normal, octahedral encoding)  69
+FLOPS_SETUP, FLOPS_TEST, FLOPS_DESCEND, FLOPS_BACKTRACK, FLOPS_FIN = 189, 82, 57, 57, 69
+PROFILE = "profiles/r2_ncu_K2_fiberA_D22.txt"  # ncu --set full summary, stamped with the .so hash
 
 
 def parse():
@@ -50,7 +76,21 @@ def parse():
     p.add_argument("--rays", type=int, default=N_RAYS)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-configs", action="store_true", help="skip C3/C4 (N = 1 only anyway)")
+    p.add_argument("--no-c5", action="store_true")
+    p.add_argument("--c5-rays", type=int, default=1 << 24)
+    p.add_argument("--c5-chunks", type=int, default=8)
+    p.add_argument("--depths", type=str, default=None, help="e.g. 2-22 or 4,9,22 (C2 sweep)")
     return p.parse_args()
+
+
+def _depths(spec):
+    if not spec:
+        return DEPTHS
+    if "-" in spec:
+        a, b = spec.split("-")
+        return tuple(range(int(a), int(b) + 1))
+    return tuple(int(x) for x in spec.split(","))
 
 
 # ------------------------------------------------------------------------------- clocks
@@ -102,24 +142,174 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------------------- workload
-def make_workloads(rank: int, n_rays: int):
-    from workloads import gen
+# ------------------------------------------------------------------------------- helpers
+def lib_sha256() -> str:
+    """Build stamp of libfiber.so: the sha256 of its SASS (cuobjdump -sass), which is
+    deterministic across builds of the same source (the .so bytes are not)."""
+    from paper_1811_03374_b200 import fiber
 
-    # rank r draws its own rays (weak scaling); rank 0 reproduces the single-GPU seeds
-    return [gen.config2(f, n_rays=n_rays, depth=22, seed={"A": 1, "B": 2, "C": 3}[f] + 1000 * rank)
-            for f in FIBERS]
+    cuobjdump = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "cuobjdump")
+    try:
+        sass = subprocess.run([cuobjdump, "-sass", fiber.LIB_PATH], capture_output=True,
+                              check=True).stdout
+        return "sass:" + hashlib.sha256(sass).hexdigest()
+    except Exception:  # noqa: BLE001
+        with open(fiber.LIB_PATH, "rb") as f:
+            return "file:" + hashlib.sha256(f.read()).hexdigest()
 
 
 def algorithmic_flops(g) -> float:
+    """Per-launch algorithmic flops from the per-pair counters in the records (flags bits
+    8-15 backtracks, 16-31 node tests) and the hit flags: a2 + a3 x tests + a4 x descents +
+    a5 x backtracks + a7 x hits, descents = tests - backtracks - 1."""
     tests = g["tests"].astype(np.float64)
     bt = g["backtracks"].astype(np.float64)
+    valid = tests > 0
     desc = np.maximum(tests - bt - 1, 0)
-    return float((FLOPS_TEST * tests + FLOPS_DESCEND * desc + FLOPS_BACKTRACK * bt).sum())
+    return float((FLOPS_SETUP * valid + FLOPS_TEST * tests + FLOPS_DESCEND * desc
+                  + FLOPS_BACKTRACK * bt + FLOPS_FIN * g["hit"]).sum())
+
+
+def device_flops(hits) -> tuple[float, float]:
+    """algorithmic_flops and the hit fraction from a device record tensor, on the device (a
+    C5 launch has 2^28 records)."""
+    import torch
+
+    f = hits.view(torch.int32)[:, 3].to(torch.int64) & 0xFFFFFFFF
+    tests = ((f >> 16) & 0xFFFF).to(torch.float64)
+    bt = ((f >> 8) & 0xFF).to(torch.float64)
+    hit = (f & 1).to(torch.float64)
+    desc = torch.clamp(tests - bt - 1, min=0)
+    fl = (FLOPS_SETUP * (tests > 0).to(torch.float64) + FLOPS_TEST * tests + FLOPS_DESCEND * desc
+          + FLOPS_BACKTRACK * bt + FLOPS_FIN * hit).sum()
+    return float(fl.item()), float(hit.mean().item())
 
 
 def fp32_peak_tflops(sms: int, mhz: float) -> float:
     return sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def profile_metrics(sha: str) -> dict:
+    """K2's metrics in the committed ncu summary, only if it was taken of this build."""
+    path = os.path.join(ROOT, PROFILE)
+    out, in_k2, stamp = {}, False, None
+    if not os.path.exists(path):
+        return {"profile": PROFILE, "profile_matches_build": False}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for line in open(path):
+        if line.startswith("# libfiber.so build stamp:"):
+            stamp = line.split(":", 1)[1].strip()
+        elif line.startswith("## "):
+            in_k2 = line.startswith("## intersect_kernel")
+        elif in_k2 and len(line.split()) >= 2:
+            parts = line.split()
+            try:
+                out[parts[0]] = float(parts[1]) * (scale.get(parts[2], 1) if len(parts) > 2 else 1)
+            except ValueError:
+                pass
+    res = {"profile": PROFILE, "profile_matches_build": stamp == sha, "profile_sha256": stamp}
+    if stamp != sha:
+        return res
+    issue = out.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
+    simt = out.get("smsp__thread_inst_executed_per_inst_executed.ratio")
+    traffic = out.get("dram__bytes_read.sum", 0.0) + out.get("dram__bytes_write.sum", 0.0)
+    res.update({"issue_active_pct": issue, "simt_lanes": simt,
+                "lane_weighted_issue_pct": round(issue * simt / 32, 2) if issue and simt else None,
+                "traffic": int(traffic) if traffic else None})
+    return res
+
+
+def _flush_fn(dev):
+    import torch
+
+    buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    return lambda: buf.fill_(1)
+
+
+def time_launches(fx, data, depth_list, steps, warmup, flush, stream, hits):
+    """Every (data index, depth) launch of a step, L2 flushed before each, with CUDA events
+    around the whole call and between its traversal and finalisation kernels.  Returns the
+    per-launch [steps, L] total and K2 times in ms."""
+    import torch
+
+    def one(record):
+        evs = []
+        for di, D in depth_list:
+            rays, segs, pairs = data[di]
+            flush()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
+            if record:
+                ev[0].record(stream)
+            fx.intersect_ex(rays, segs, pairs, D, hits=hits[:pairs.shape[0]],
+                            event_after_traverse=ev[1] if record else None)
+            if record:
+                ev[2].record(stream)
+                evs.append(ev)
+        return evs
+
+    for _ in range(warmup):
+        one(False)
+    torch.cuda.synchronize()
+    all_ev = [one(True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    tot = np.array([[e[0].elapsed_time(e[2]) for e in s] for s in all_ev])
+    k2 = np.array([[e[0].elapsed_time(e[1]) for e in s] for s in all_ev])
+    return tot, k2
+
+
+def roofline(flops, k2_ms, peak, prof, n_pairs, bytes_per_pair):
+    ach = flops / (k2_ms * 1e-3) / 1e12
+    r = {"bound": "alu", "achieved": round(ach, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+         "frac": round(ach / peak, 4), "traffic": prof.get("traffic"),
+         "flops_per_pair": round(flops / n_pairs, 1),
+         "algorithmic_bytes_per_launch": int(bytes_per_pair * n_pairs)}
+    for k in ("issue_active_pct", "simt_lanes", "lane_weighted_issue_pct", "profile",
+              "profile_matches_build"):
+        if k in prof:
+            r[k] = prof[k]
+    return r
+
+
+# ------------------------------------------------------------------------------- ranks
+# One process per GPU over NCCL.  Test hook: FIBER_BENCH_GLOO_1GPU=1 runs the ranks with the
+# gloo backend, all on cuda:0 (their kernels never wait on one another; only host-side
+# collectives synchronise), to exercise the N > 1 code path on a one-GPU box.
+GLOO_1GPU = os.environ.get("FIBER_BENCH_GLOO_1GPU") == "1"
+
+
+def _max_over_ranks(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if GLOO_1GPU else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x: int, dev) -> int:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return x
+    t = torch.tensor([x], dtype=torch.int64, device="cpu" if GLOO_1GPU else dev)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def _gather_rows(row, dev) -> np.ndarray:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(row, dtype=torch.float64)
+    if not (dist.is_available() and dist.is_initialized()):
+        return t.numpy()[None]
+    t = t if GLOO_1GPU else t.to(dev)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return torch.stack(out).cpu().numpy()
 
 
 # ------------------------------------------------------------------------------- ours
@@ -132,58 +322,44 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if GLOO_1GPU:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if GLOO_1GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     fx.lib()
-    wls = make_workloads(rank, args.rays)
+    sha = lib_sha256()
+    prof = profile_metrics(sha)
+    depths = _depths(args.depths)
+    from workloads import gen
+
+    # rank r draws its own rays (weak scaling); rank 0 reproduces the single-GPU seeds
+    wls = [gen.config2(f, n_rays=args.rays, depth=22, seed={"A": 1, "B": 2, "C": 3}[f] + 1000 * rank)
+           for f in FIBERS]
     data = [fx.to_device(w, dev) for w in wls]
     n = args.rays
     hits = torch.empty((n, 4), dtype=torch.float32, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = _flush_fn(dev)
     stream = torch.cuda.current_stream()
-    launches = [(fi, D) for fi in range(len(FIBERS)) for D in DEPTHS]
+    launches = [(fi, D) for fi in range(len(FIBERS)) for D in depths]
     pairs_per_step = n * len(launches)
 
-    def step(record):
-        # one fiber_intersect per (fiber, depth), issued as its two stages so that the
-        # traversal kernel (K2, the dominant one) is timed on its own
-        ms = []
-        for fi, D in launches:
-            rays, segs, pairs = data[fi]
-            flush.fill_(1)  # untimed L2 flush: inputs come from HBM
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
-            if record:
-                ev[0].record(stream)
-            fx.intersect_ex(rays, segs, pairs, D, hits=hits,
-                            event_after_traverse=ev[1] if record else None)
-            if record:
-                ev[2].record(stream)
-                ms.append(ev)
-        return ms
-
-    for _ in range(args.warmup):
-        step(False)
-    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     with ClockSampler(local) as clk:
-        evs = [step(True) for _ in range(args.steps)]
-        torch.cuda.synchronize()
+        per_launch, per_k2 = time_launches(fx, data, launches, args.steps, args.warmup, flush,
+                                           stream, hits)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    per_launch = np.array([[e[0].elapsed_time(e[2]) for e in s] for s in evs])  # [K, 63] ms
-    per_k2 = np.array([[e[0].elapsed_time(e[1]) for e in s] for s in evs])
-    total_ms = float(per_launch.sum())
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = _max_over_ranks(float(per_launch.sum()), dev)
     value = world * pairs_per_step * args.steps / (total_ms * 1e-3) / 1e9
 
     # per-launch counters (deterministic) for the algorithmic flop count, by depth
@@ -194,9 +370,9 @@ def run_ours(args):
         g = fx.unpack(fx.intersect(rays, segs, pairs, D))
         flops[j] = algorithmic_flops(g)
         hitfrac[j] = g["hit"].mean()
-    mean_ms = per_launch.mean(0)  # per launch, over steps
+    mean_ms = per_launch.mean(0)
     by_depth = {}
-    for D in DEPTHS:
+    for D in depths:
         idx = [j for j, (fi, d) in enumerate(launches) if d == D]
         by_depth[str(D)] = round(n * len(idx) / (mean_ms[idx].sum() * 1e-3) / 1e9, 3)
     clocks = clk.summary()
@@ -204,65 +380,157 @@ def run_ours(args):
     peak_mhz = clocks["sm_max_mhz"] or 1965.0
     peak = fp32_peak_tflops(sms, peak_mhz)
     k2_ms = per_k2.mean(0)
-    achieved = float(flops.sum() / (k2_ms.sum() * 1e-3) / 1e12)
-
-    # gather per-ray hit records across ranks (the one collective)
-    gather_ms = None
-    if world > 1:
-        from paper_1811_03374_b200 import dist as fxd
-
-        gather_ms = fxd.timed_gather(hits)
-
+    roof = roofline(float(flops.sum()), float(k2_ms.sum()), peak, prof, pairs_per_step, 56)
+    roof["algorithmic_bytes_per_launch"] = 56 * n  # 8 B pair + 32 B ray + 16 B record per pair
+    roof.update({"peak_basis": f"FP32: {sms} SMs x 128 lanes x 2 x {peak_mhz:.0f} MHz (max SM "
+                               "clock; B200_PROFILING.md unit counts)",
+                 "kernel": "intersect_kernel (K2), CUDA events on its stream, whole C2 sweep",
+                 "k2_share_of_step": round(float(k2_ms.sum() / mean_ms.sum()), 3),
+                 "flops_note": "per pair: 189 (a2) + 82 x tests + 57 x descents + 57 x "
+                               "backtracks + 69 x hit (a7), counters from the records"})
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded; workloads/gen.py config2)",
+        "data": "synthetic (seeded; workloads/gen.py config2..5)",
         "config": {"workload": "C2: single cubic fiber x 2^20 random rays, fibers F_A/F_B/F_C, "
                                "depth sweep 2-22 (Fig. 1 shape)",
-                   "rays_per_fiber_per_rank": n, "depths": [DEPTHS[0], DEPTHS[-1]],
+                   "rays_per_fiber_per_rank": n, "depths": [depths[0], depths[-1]],
                    "launches_per_step": len(launches), "tests_per_step_per_rank": pairs_per_step,
                    "l2": "flushed (256 MiB write) before every timed launch",
                    "parallelism": f"ray-sharded x{world}"},
         "by_depth": by_depth,
-        "drop_4_22": round(by_depth["4"] / by_depth["22"], 3),
+        "drop_4_22": round(by_depth["4"] / by_depth["22"], 3) if "4" in by_depth and "22" in by_depth else None,
         "hit_fraction_by_depth": {str(D): round(float(np.mean(
-            [hitfrac[j] for j, (fi, d) in enumerate(launches) if d == D])), 4) for D in DEPTHS},
-        "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                     "traffic": _k2_traffic(),
-                     "issue_active_pct": _k2_profile_metrics().get(
-                         "smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                     "simt_lanes": _k2_profile_metrics().get(
-                         "smsp__thread_inst_executed_per_inst_executed.ratio"),
-                     "algorithmic_bytes_per_launch": 56 * n,
-                     "peak_basis": f"FP32: {sms} SMs x 128 lanes x 2 x {peak_mhz:.0f} MHz "
-                                   "(max SM clock; B200_PROFILING.md unit counts)",
-                     "kernel": "intersect_kernel (K2), timed alone with CUDA events",
-                     "k2_share_of_step": round(float(k2_ms.sum() / mean_ms.sum()), 3),
-                     "traffic_note": "traffic, issue_active_pct and simt_lanes: one K2 launch "
-                                     "(fiber A, D=22, 2^20 pairs) in the committed ncu --set full "
-                                     "summary " + TRAFFIC_PROFILE + "; the kernel is bound by "
-                                     "instruction issue (comparisons, selects, MUFU), not by "
-                                     "FP32 flops"},
+            [hitfrac[j] for j, (fi, d) in enumerate(launches) if d == D])), 4) for D in depths},
+        "roofline": roof,
         "gpu_launches": args.steps * len(launches) * 2,
         "clocks": clocks,
         "wall_s_timed": round(wall, 3),
+        "libfiber_build_stamp": sha,
     }
-    if gather_ms is not None:
-        out["gather_ms"] = gather_ms
+    samples = {}
+    if world == 1 and not args.no_configs:
+        out["configs"], samples = run_configs(args, fx, dev, flush, stream, peak, prof)
+        out["gpu_launches"] += sum(2 * args.steps for _ in out["configs"])
+    if not args.no_c5:
+        out["c5"], c5_sample = run_c5(args, fx, dev, world, rank, peak)
+        out["gpu_launches"] += out["c5"].pop("_launches")
+        if c5_sample is not None:
+            samples["C5"] = c5_sample
     if not args.no_e2e:
-        out["e2e"] = e2e(args, fx, wls, dev)
+        out["e2e"] = e2e(args, fx, wls, dev, depths)
     if rank == 0 and not args.no_cpu and world == 1:
-        out["cpu_baseline"] = cpu_baseline()
+        out["cpu_baseline"] = cpu_baseline(samples)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def e2e(args, fx, wls, dev):
+def run_configs(args, fx, dev, flush, stream, peak, prof):
+    """BASELINE configs 3 and 4 at full size (N = 1): device-timed like the C2 launches."""
+    import torch
+
+    from workloads import gen
+
+    res, samples = {}, {}
+    for name, make, bpp in (("C3", lambda: gen.config3(device=dev), 26.4),
+                            ("C4", lambda: gen.config4(device=dev), 56.0)):
+        t_gen = time.perf_counter()
+        w = make()
+        t_gen = time.perf_counter() - t_gen
+        rays, segs, pairs = fx.to_device(w, dev)
+        hits = torch.empty((w.n_pairs, 4), dtype=torch.float32, device=dev)
+        tot, k2 = time_launches(fx, [(rays, segs, pairs)], [(0, w.depth)], args.steps,
+                                max(args.warmup, 1), flush, stream, hits)
+        fx.intersect(rays, segs, pairs, w.depth, hits=hits)
+        flops, hitf = device_flops(hits)
+        tests_pp = float(((hits.view(torch.int32)[:, 3].to(torch.int64) >> 16) & 0xFFFF)
+                         .to(torch.float64).mean().item())
+        ms, ms_k2 = float(np.median(tot)), float(np.median(k2))
+        res[name] = {"workload": w.name, "pairs": w.n_pairs, "depth": w.depth,
+                     "value": round(w.n_pairs / (ms * 1e-3) / 1e9, 3), "unit": UNIT,
+                     "ms": round(ms, 4), "k2_ms": round(ms_k2, 4),
+                     "k3_share": round(1 - ms_k2 / ms, 3),
+                     "hit_fraction": round(hitf, 4),
+                     "tests_per_pair": round(tests_pp, 3),
+                     "roofline": roofline(flops, ms_k2, peak, {}, w.n_pairs, bpp),
+                     "gen_s": round(t_gen, 1)}
+        rng = np.random.default_rng(17)
+        sub = np.sort(rng.choice(w.n_pairs, 2048, replace=False))
+        samples[name] = (w.subsample_idx(sub),
+                         fx.unpack(hits[torch.from_numpy(sub).to(dev)]))
+        del rays, segs, pairs, hits
+        torch.cuda.empty_cache()
+    return res, samples
+
+
+def run_c5(args, fx, dev, world, rank, peak):
+    """BASELINE config 5, strong-scaled: 2^24 fur rays x 16 candidates = 2^28 pairs in total,
+    D = 6, rays shuffled and blocked over the ranks; per rank K chunk launches of the nearest
+    epilogue with the per-ray records all-gathered on a second stream (ShardedNearest)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_03374_b200 import dist as fxd
+    from workloads import gen
+
+    n_rays, K = args.c5_rays, args.c5_chunks
+    perm = fxd.ray_permutation(n_rays, seed=5)
+    a, b = fxd.shard_bounds(n_rays, world, rank)
+    owned = perm[a:b]
+    t_gen = time.perf_counter()
+    w = gen.config5(n_rays=n_rays, ray_ids=owned, device=dev)
+    pairs, bounds, blocks = fxd.chunk_by_ray(w.pairs, owned, n_rays, K, device=dev)
+    t_gen = time.perf_counter() - t_gen
+    rays = torch.from_numpy(w.rays).to(dev)
+    segs = fx.build_segments(torch.from_numpy(w.ctrl).to(dev), torch.from_numpy(w.radii).to(dev))
+    sn = fxd.ShardedNearest(fx, rays, segs, pairs, bounds, blocks, w.depth, dev)
+    for _ in range(max(args.warmup, 1)):
+        sn.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kern, tot = [], []
+    for _ in range(args.steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        sn.step(ev)
+        torch.cuda.synchronize()
+        kern.append(ev[0].elapsed_time(ev[1]))
+        tot.append(ev[0].elapsed_time(ev[2]))
+    if world > 1:
+        dist.barrier()
+    k_ms, e_ms = float(np.median(kern)), float(np.median(tot))
+    allr = _gather_rows([k_ms, e_ms], dev)
+    n_total = _sum_over_ranks(int(pairs.shape[0]), dev)
+    flops, hitf = device_flops(sn.hits)
+    res = {"workload": f"C5: fur 2^21 segments, {n_rays} targeted rays x 16 candidates, D={w.depth}, "
+                       f"rays shuffled and blocked over {world} rank(s), {K} chunk launches per rank",
+           "pairs_total": n_total, "pairs_this_rank": int(pairs.shape[0]),
+           "value": round(n_total / (allr[:, 1].max() * 1e-3) / 1e9, 3), "unit": UNIT,
+           "kernel_value": round(n_total / (allr[:, 0].max() * 1e-3) / 1e9, 3),
+           "ms": round(float(allr[:, 1].max()), 4), "kernel_ms": round(float(allr[:, 0].max()), 4),
+           "gather_ms_exposed": round(float((allr[:, 1] - allr[:, 0]).max()), 4),
+           "rank_kernel_ms_max_over_mean": round(float(allr[:, 0].max() / allr[:, 0].mean()), 4),
+           "scaling": "strong",
+           "collective": (None if world == 1 else "gloo all_gather (test hook, 1 GPU)" if GLOO_1GPU
+                          else "NCCL all_gather_into_tensor per chunk"),
+           "records_bytes_gathered": int(16 * n_rays) if world > 1 else 0,
+           "hit_fraction": round(hitf, 4),
+           "roofline": roofline(flops, float(np.median(kern)), peak, {}, pairs.shape[0], 26.4),
+           "gen_s": round(t_gen, 1), "_launches": args.steps * (2 * K + 1)}
+    sample = None
+    if rank == 0 and world == 1:
+        rng = np.random.default_rng(19)
+        sub = np.sort(rng.choice(pairs.shape[0], 2048, replace=False))
+        wp = gen.Workload(w.name, w.rays, w.ctrl, w.radii, pairs[sub], w.depth)
+        sample = (wp, fx.unpack(sn.hits[torch.from_numpy(sub).to(dev)]))
+    return res, sample
+
+
+def e2e(args, fx, wls, dev, depths=DEPTHS):
     """Same metric through the public API with HOST buffers: every step copies each fiber's
     rays, pairs and segment host->device (pinned) and brings every launch's result back to the
     host: its hit records in pair order (fiber_compact_hits: the records with FIBER_HIT and
@@ -337,7 +605,7 @@ def e2e(args, fx, wls, dev):
         for f in range(nb):
             d_rays, d_pairs, d_ctrl, d_rad = d_in[f]
             segs = None
-            for D in DEPTHS:
+            for D in depths:
                 s, cs = j % R, comps[j % NC]
                 with torch.cuda.stream(cs):
                     cs.wait_event(ev_in[f])
@@ -387,10 +655,8 @@ def e2e(args, fx, wls, dev):
     if torch.distributed.is_available() and torch.distributed.is_initialized():
         # whole-job number: every rank's tests over the slowest rank's time
         world = torch.distributed.get_world_size()
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    tests = world * n * len(FIBERS) * len(DEPTHS) * k
+        ms = _max_over_ranks(ms, dev)
+    tests = world * n * len(FIBERS) * len(depths) * k
     return {"value": round(tests / (ms * 1e-3) / 1e9, 4), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(ms / k, 3), "steps": k,
@@ -398,6 +664,7 @@ def e2e(args, fx, wls, dev):
             "note": "results = per launch the hit records in pair order + their pair indices "
                     "(fiber_compact_hits) + the count; launches alternate between 2 compute "
                     "streams, copies on two copy streams overlapping them (ring of 8 result slots)"}
+
 
 
 # ------------------------------------------------------------------------------- oracle
@@ -424,45 +691,32 @@ def _time_oracle(ws, nthreads):
     return n, time.perf_counter() - t0
 
 
-TRAFFIC_PROFILE = "profiles/r1_full_K2K3_fiberA_D22.txt"
-
-
-def _k2_profile_metrics() -> dict:
-    """K2's metrics in the committed ncu --set full summary (TRAFFIC_PROFILE), by name."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), TRAFFIC_PROFILE)
-    out, in_k2 = {}, False
-    if not os.path.exists(path):
-        return out
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for line in open(path):
-        if line.startswith("## "):
-            in_k2 = line.startswith("## intersect_kernel")
-        elif in_k2 and len(line.split()) >= 2:
-            parts = line.split()
-            try:
-                out[parts[0]] = float(parts[1]) * (scale.get(parts[2], 1) if len(parts) > 2 else 1)
-            except ValueError:
-                pass
-    return out
-
-
-def _k2_traffic():
-    """DRAM bytes (read + write) of one K2 launch from the committed ncu summary, or None."""
-    m = _k2_profile_metrics()
-    t = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-    return int(t) if t else None
-
-
-def cpu_baseline(n_per: int = 1 << 17):
+def cpu_baseline(samples: dict, n_per: int = 1 << 17):
+    """The FP64 oracle as it stands, timed on a C2 subsample (the reported baseline), then run
+    on the 2,048-pair samples of C3, C4 and C5 that the GPU records above were taken for: its
+    time per pair there, and the parity of those GPU records against it (tests/parity.py)."""
     import oracle
+    from tests.parity import compare
 
     oracle.build()
     cores = os.cpu_count() or 1
     ws = _oracle_sample(n_per)
     n, el = _time_oracle(ws, cores)
-    return {"value": n / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"C2 subsample: {n_per} of 2^20 rays per fiber x 3 fibers x depths 2-22 "
-                      f"= {n} tests, FP64 oracle without the eps runs, {el:.2f} s wall"}
+    out = {"value": n / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"C2 subsample: {n_per} of 2^20 rays per fiber x 3 fibers x depths 2-22 "
+                     f"= {n} tests, FP64 oracle without the eps runs, {el:.2f} s wall"}
+    par = {}
+    for name, (w, g) in samples.items():
+        t0 = time.perf_counter()
+        o = oracle.intersect(w.rays, w.ctrl, w.radii, w.pairs, w.depth, nthreads=cores)
+        el = time.perf_counter() - t0
+        rep = compare(g, o)
+        par[name] = {k: rep[k] for k in ("n", "hits", "grazing", "hit_mismatch", "compared",
+                                         "excluded_values", "value_mismatch", "max_t_rel",
+                                         "max_u", "max_angle")}
+        par[name]["oracle_G_tests_per_s_with_eps_runs"] = round(w.n_pairs / el / 1e9, 6)
+    out["sampled_parity"] = par
+    return out
 
 
 def run_reference(args):
@@ -499,9 +753,32 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-if __name__ == "__main__":
+# ------------------------------------------------------------------------------- launcher
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def main():
     a = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and a.gpus > 1:
+        # --gpus N without a torchrun environment: launch N ranks (one per GPU) ourselves
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world_env is not None and int(world_env) != a.gpus:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world_env}\n")
+        sys.exit(2)
     if a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

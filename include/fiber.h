@@ -289,6 +289,19 @@ int fiber_compact_hits(const fiber_hit *hits, int64_t n, fiber_hit *out, uint32_
 /* Fill nearest[0..n_rays) with the "no hit" key (all ones). */
 int fiber_nearest_init(uint64_t *nearest, int64_t n_rays, void *cuda_stream);
 
+/* Per-ray records of the nearest-hit epilogue (the records a multi-GPU
+ * run gathers, 16 B per ray).  For j in [0, n): r = ray_ids[j], key = nearest[r] (as written by
+ * fiber_intersect_nearest over `pairs` / `hits` of ONE launch, the key's low word is the pair
+ * index in it):
+ *   key == all ones (no hit): out[j] = {t = +inf, u = 0, n_oct = 0, flags = 0xffffffff}
+ *   else i = key & 0xffffffff: out[j] = {hits[i].t, hits[i].u, hits[i].n_oct, pairs[i].seg}
+ * i.e. the record of the ray's first hit with the hit segment's index in place of the flags.
+ *   nearest  device uint64[>= max ray id + 1];  hits, pairs  device, of the launch
+ *   ray_ids  device int64[n];  out  device fiber_hit[n] (may not alias the inputs)
+ * Errors: FIBER_EINVAL (n < 0, NULL with n > 0), FIBER_EDEVICE, FIBER_ECUDA. */
+int fiber_nearest_records(const uint64_t *nearest, const fiber_hit *hits, const fiber_pair *pairs,
+                          const int64_t *ray_ids, int64_t n, fiber_hit *out, void *cuda_stream);
+
 /* Static description of the last failure on this thread (or of `code`). */
 const char *fiber_error_string(int code);
 

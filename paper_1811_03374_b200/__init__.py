@@ -6,6 +6,7 @@ The product path is libfiber.so (CUDA C ABI, include/fiber.h) behind the ctypes 
 from .fiber import (BAD_INPUT, BAD_SEGMENT, HIT, INSIDE, Grid, KIND_CAP0, KIND_CAP1, KIND_LATERAL,  # noqa: F401
                     KIND_WEDGE, MAX_DEPTH, FiberError, Segments, build_segments, build_segments_quadratic,
                     compact_hits, decode_normals,
-                    intersect, intersect_closest, intersect_ex, intersect_nearest, lib, nearest_init, presplit,
+                    intersect, intersect_closest, intersect_ex, intersect_nearest, lib, nearest_init,
+                    nearest_records, presplit,
                     remap_u, to_device,
                     unpack)

@@ -104,3 +104,41 @@ extern "C" int fiber_compact_hits(const fiber_hit* hits, int64_t n, fiber_hit* o
   cudaFreeAsync(sums, st);
   return rc;
 }
+
+// ------------------------------------------------------------------------------------
+// fiber_nearest_records: the per-ray records of the nearest-hit epilogue (include/fiber.h)
+// ------------------------------------------------------------------------------------
+namespace fibercompact {
+__global__ void records_kernel(const unsigned long long* __restrict__ nearest,
+                               const uint4* __restrict__ hits, const uint2* __restrict__ pairs,
+                               const int64_t* __restrict__ ray_ids, int64_t n,
+                               uint4* __restrict__ out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = nearest[__ldg(&ray_ids[j])];
+    uint4 r = make_uint4(0x7f800000u, 0u, 0u, 0xffffffffu);  // +inf, no hit
+    if (key != ~0ull) {
+      const uint32_t i = (uint32_t)key;
+      r = __ldg(&hits[i]);
+      r.w = __ldg(&pairs[i]).y;
+    }
+    out[j] = r;
+  }
+}
+}  // namespace fibercompact
+
+extern "C" int fiber_nearest_records(const uint64_t* nearest, const fiber_hit* hits,
+                                     const fiber_pair* pairs, const int64_t* ray_ids, int64_t n,
+                                     fiber_hit* out, void* cuda_stream) {
+  if (n < 0 || (n > 0 && (!nearest || !hits || !pairs || !ray_ids || !out)))
+    return set_error(FIBER_EINVAL, "fiber_nearest_records: bad arguments");
+  int rc = check_device();
+  if (rc != FIBER_OK) return rc;
+  if (n == 0) return FIBER_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  fibercompact::records_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)cuda_stream>>>(
+      (const unsigned long long*)nearest, (const uint4*)hits, (const uint2*)pairs, ray_ids, n,
+      (uint4*)out);
+  return check_launch("fiber_nearest_records");
+}

@@ -34,23 +34,6 @@ def shard_pairs(pairs: np.ndarray, n_rays: int, world: int, rank: int, seed: int
     return np.ascontiguousarray(local[order]), owned
 
 
-def nearest_records(nearest_keys: torch.Tensor, hits: torch.Tensor, pairs: torch.Tensor,
-                    rays: torch.Tensor) -> torch.Tensor:
-    """Per-ray record (t, u, n_oct, seg) from the fused nearest-hit keys; misses get
-    t = +inf and seg = -1.  `rays` are the (global) ray ids the keys are indexed by."""
-    keys = nearest_keys[rays]
-    hit = keys != -1
-    idx = torch.where(hit, keys & 0xFFFFFFFF, torch.zeros_like(keys))
-    rec = hits[idx].clone()
-    seg = pairs[idx, 1].clone()
-    rec[~hit, 0] = float("inf")
-    rec[~hit, 1] = 0.0
-    rec[~hit, 2] = 0.0
-    rec_i = rec.view(torch.int32)
-    rec_i[:, 3] = torch.where(hit, seg, torch.full_like(seg, -1))
-    return rec
-
-
 def gather_records(local: torch.Tensor) -> torch.Tensor:
     """all_gather of equally sized per-rank record blocks -> [world * n_local, ...]
     (one NCCL all_gather_into_tensor on GPUs; list all_gather on gloo)."""
@@ -92,3 +75,97 @@ def timed_gather(local: torch.Tensor, iters: int = 3) -> float:
     t = torch.tensor([e0.elapsed_time(e1) / iters], device=local.device, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return round(float(t.item()), 4)
+
+
+def chunk_by_ray(pairs: np.ndarray, owned: np.ndarray, n_rays: int, n_chunks: int,
+                 device=None):
+    """Split a rank's pairs into n_chunks launches by blocks of its owned rays (shard order):
+    chunk k holds every pair of owned[k m / K : (k+1) m / K], in the input's order within the
+    chunk (so pairs sorted by segment stay so).  Returns (pairs reordered, chunk bounds [K+1],
+    owned ray blocks [K]).  device: sort there (torch)."""
+    m = len(owned)
+    pos = np.full(n_rays, -1, dtype=np.int64)
+    pos[owned] = np.arange(m)
+    starts = np.array([k * m // n_chunks for k in range(n_chunks)], dtype=np.int64)
+    pp = pos[pairs[:, 0].astype(np.int64)]
+    if (pp < 0).any():
+        raise ValueError("chunk_by_ray: a pair's ray is not owned by this rank")
+    ck = np.searchsorted(starts, pp, side="right") - 1
+    if (ck < 0).any():
+        raise ValueError("chunk_by_ray: a pair's ray is not owned by this rank")
+    if device is not None:  # the stable sort of 2^28 keys (C5) on the GPU
+        order = torch.sort(torch.from_numpy(ck).to(device), stable=True).indices.cpu().numpy()
+    else:
+        order = np.argsort(ck, kind="stable")
+    counts = np.bincount(ck, minlength=n_chunks)
+    bounds = np.concatenate([[0], np.cumsum(counts)])
+    blocks = [owned[k * m // n_chunks:(k + 1) * m // n_chunks] for k in range(n_chunks)]
+    return np.ascontiguousarray(pairs[order]), bounds, blocks
+
+
+class ShardedNearest:
+    """The multi-GPU path of SURVEY 8(e): this rank's ray shard, its pairs in K chunk launches of
+    fiber_intersect_nearest (K2 + the per-ray nearest epilogue) on a compute stream, and per
+    chunk -- as soon as its launch is done, on a second stream -- its per-ray records
+    (fiber_nearest_records) gathered from every rank with one all_gather_into_tensor, so chunk k's
+    exchange overlaps chunk k+1's kernels.  No other data crosses ranks: rays and segments are
+    replicated, per-pair records stay on their GPU.  records[k] ends as [world x block_k, 4]
+    (rank-major), the rays of rank r's block k."""
+
+    def __init__(self, fx, rays, segs, pairs: np.ndarray, bounds, blocks, depth: int, device):
+        self.fx, self.rays, self.segs, self.depth = fx, rays, segs, depth
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.pairs = torch.from_numpy(pairs.view(np.int32)).to(device)
+        self.hits = torch.empty((pairs.shape[0], 4), dtype=torch.float32, device=device)
+        self.nearest = torch.empty(rays.shape[0], dtype=torch.int64, device=device)
+        self.bounds = [int(b) for b in bounds]
+        self.blocks = [torch.from_numpy(np.asarray(b, dtype=np.int64)).to(device) for b in blocks]
+        self.out = [torch.empty((self.world * len(b), 4), dtype=torch.float32, device=device)
+                    for b in blocks]
+        self.compute = torch.cuda.Stream(device=device)
+        self.comm = torch.cuda.Stream(device=device)
+        self.done = [torch.cuda.Event() for _ in blocks]
+        self.nccl = self.world > 1 and dist.get_backend() == "nccl"
+
+    def step(self, events=None):
+        """One pass over this rank's pairs.  events = (start, kernels_done, all_done) timing
+        events: start and kernels_done on the compute stream, all_done on the comm stream."""
+        cur = torch.cuda.current_stream()
+        self.compute.wait_stream(cur)
+        self.comm.wait_stream(cur)
+        with torch.cuda.stream(self.compute):
+            if events:
+                events[0].record(self.compute)
+            self.fx.nearest_init(self.nearest, stream=self.compute)
+            for k in range(len(self.blocks)):
+                a, b = self.bounds[k], self.bounds[k + 1]
+                self.fx.intersect_nearest(self.rays, self.segs, self.pairs[a:b], self.depth,
+                                          self.nearest, hits=self.hits[a:b], stream=self.compute)
+                self.done[k].record(self.compute)
+            if events:
+                events[1].record(self.compute)
+        with torch.cuda.stream(self.comm):
+            for k in range(len(self.blocks)):
+                a, b = self.bounds[k], self.bounds[k + 1]
+                self.comm.wait_event(self.done[k])
+                rec = self.fx.nearest_records(self.nearest, self.hits[a:b], self.pairs[a:b],
+                                              self.blocks[k], stream=self.comm)
+                if self.nccl:
+                    dist.all_gather_into_tensor(self.out[k], rec)
+                elif self.world > 1:
+                    self.out[k].copy_(gather_records(rec.cpu()).to(rec.device))
+                else:
+                    self.out[k].copy_(rec)
+            if events:
+                events[2].record(self.comm)
+        cur.wait_stream(self.compute)
+        cur.wait_stream(self.comm)
+
+    def records_by_ray(self, n_rays: int, all_blocks) -> torch.Tensor:
+        """The gathered records scattered to ray order: all_blocks[r][k] = rank r's block k."""
+        out = torch.full((n_rays, 4), float("nan"), dtype=torch.float32, device=self.out[0].device)
+        for k in range(len(self.blocks)):
+            ids = torch.cat([torch.as_tensor(np.asarray(all_blocks[r][k]), dtype=torch.int64)
+                             for r in range(self.world)]).to(out.device)
+            out[ids] = self.out[k]
+        return out

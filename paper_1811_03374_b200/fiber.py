@@ -35,7 +35,8 @@ EXPORTS = ("fiber_segments_bytes", "fiber_segments_view", "fiber_build_segments"
            "fiber_grid_count", "fiber_grid_candidates", "fiber_grid_closest",
            "fiber_intersect", "fiber_intersect_nearest", "fiber_intersect_closest",
            "fiber_intersect_ex", "fiber_compact_hits",
-           "fiber_nearest_init", "fiber_error_string", "fiber_decode_normal", "fiber_abi_version")
+           "fiber_nearest_init", "fiber_nearest_records", "fiber_error_string",
+           "fiber_decode_normal", "fiber_abi_version")
 
 
 class FiberError(RuntimeError):
@@ -84,6 +85,7 @@ def lib() -> ctypes.CDLL:
         L.fiber_intersect_closest.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64,
                                               ctypes.c_int, vp, vp, vp]
         L.fiber_nearest_init.argtypes = [vp, i64, vp]
+        L.fiber_nearest_records.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         L.fiber_compact_hits.argtypes = [vp, i64, vp, vp, vp, vp]
         L.fiber_intersect_ex.argtypes = [vp, i64, ctypes.POINTER(_Segs), vp, i64, ctypes.c_int,
                                          vp, vp, vp, vp]
@@ -93,7 +95,8 @@ def lib() -> ctypes.CDLL:
                   "fiber_build_segments_quadratic", "fiber_presplit_count",
                   "fiber_presplit_write", "fiber_remap_u", "fiber_grid_create",
                   "fiber_grid_destroy", "fiber_grid_info", "fiber_grid_count",
-                  "fiber_grid_candidates", "fiber_grid_closest", "fiber_compact_hits"):
+                  "fiber_grid_candidates", "fiber_grid_closest", "fiber_compact_hits",
+                  "fiber_nearest_records"):
             getattr(L, f).restype = ctypes.c_int
         L.fiber_error_string.argtypes = [ctypes.c_int]
         L.fiber_error_string.restype = ctypes.c_char_p
@@ -443,6 +446,29 @@ def nearest_init(nearest: torch.Tensor, stream=None) -> torch.Tensor:
     _check(lib().fiber_nearest_init(nearest.data_ptr(), nearest.numel(), _stream(stream)),
            "fiber_nearest_init")
     return nearest
+
+
+def nearest_records(nearest: torch.Tensor, hits: torch.Tensor, pairs: torch.Tensor,
+                    ray_ids: torch.Tensor, out: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+    """fiber_nearest_records: per-ray records (t, u, n_oct, segment; misses t = +inf, segment
+    = -1) of the rays `ray_ids` from one nearest-hit launch's keys, records and pairs."""
+    with _on(stream):
+        pairs = _pairs(pairs)
+        _hits(hits, pairs.shape[0], pairs.device)
+        if not (nearest.is_cuda and nearest.dtype == torch.int64 and nearest.is_contiguous()):
+            raise FiberError("nearest must be a contiguous CUDA int64 tensor")
+        ray_ids = ray_ids.to(torch.int64).contiguous()
+        if not ray_ids.is_cuda or ray_ids.device != pairs.device:
+            raise FiberError("ray_ids must be a CUDA tensor on the pairs' device")
+        n = ray_ids.numel()
+        if out is None:
+            out = torch.empty((n, 4), dtype=torch.float32, device=pairs.device)
+        _hits(out, n, pairs.device, "out")
+        _check(lib().fiber_nearest_records(nearest.data_ptr(), hits.data_ptr(), pairs.data_ptr(),
+                                           ray_ids.data_ptr(), n, out.data_ptr(), _stream(stream)),
+               "fiber_nearest_records")
+    return out
 
 
 # ------------------------------------------------------------------------- host helpers

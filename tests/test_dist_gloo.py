@@ -108,3 +108,22 @@ def test_sharded_nearest_records_equal_single_process():
     assert np.array_equal(np.isinf(got[:, 0]), np.isinf(exp[:, 0]))
     fin = np.isfinite(exp[:, 0])
     assert np.array_equal(got[fin], exp[fin])  # bit-identical records
+
+
+def test_chunk_by_ray_partitions_the_shard():
+    rays, ctrl, radii, pairs = _workload()
+    n = rays.shape[0]
+    for world in (1, 2, 4):
+        for rank in range(world):
+            local, owned = fxd.shard_pairs(pairs, n, world, rank, seed=3)
+            for K in (1, 3, 8):
+                cp, bounds, blocks = fxd.chunk_by_ray(local, owned, n, K)
+                assert bounds[0] == 0 and bounds[-1] == local.shape[0]
+                assert np.array_equal(np.sort(np.concatenate(blocks)), np.sort(owned))
+                for k in range(K):
+                    ck = cp[bounds[k]:bounds[k + 1]]
+                    assert set(ck[:, 0].tolist()) <= set(blocks[k].tolist())
+                    # the (segment, ray) order of the shard survives within every chunk
+                    key = ck[:, 1].astype(np.int64) << 32 | ck[:, 0].astype(np.int64)
+                    assert np.all(np.diff(key) >= 0)
+                assert sorted(map(tuple, cp.tolist())) == sorted(map(tuple, local.tolist()))

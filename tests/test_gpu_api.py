@@ -63,6 +63,17 @@ def test_nearest_epilogue_matches_host_mirror(fx):
     exp = fxd.nearest_keys_host(g["t"], g["hit"], pairs_np, n_rays)
     assert np.array_equal(near.cpu().numpy(), exp)
     assert (exp >= 0).sum() > 500
+    # per-ray records (fiber_nearest_records) of a shuffled subset of the rays
+    ids = np.random.default_rng(2).permutation(n_rays)[:3000]
+    rec = fx.nearest_records(near, hits, pairs, torch.from_numpy(ids).cuda()).cpu().numpy()
+    hn = hits.cpu().numpy()
+    for j, r in enumerate(ids):
+        if exp[r] < 0:
+            assert np.isinf(rec[j, 0]) and rec[j, 1] == 0 and rec[j].view(np.uint32)[3] == 0xFFFFFFFF
+        else:
+            i = int(exp[r]) & 0xFFFFFFFF
+            assert np.array_equal(rec[j, :3].view(np.uint32), hn[i, :3].view(np.uint32))
+            assert rec[j].view(np.uint32)[3] == pairs_np[i, 1]
     # nearest-only (no hits buffer): the library uses scratch records
     near2 = torch.empty_like(near)
     fx.nearest_init(near2)

@@ -52,6 +52,11 @@ class Workload:
             h.update(np.ascontiguousarray(a).tobytes())
         return h.hexdigest()
 
+    def subsample_idx(self, idx: np.ndarray) -> "Workload":
+        """The pairs at the given indices (same rays/segments arrays)."""
+        return Workload(self.name + f"[{len(idx)} pairs]", self.rays, self.ctrl, self.radii,
+                        np.ascontiguousarray(self.pairs[idx]), self.depth, dict(self.meta))
+
     def subsample(self, n: int, seed: int = 12345) -> "Workload":
         """Seeded subsample of n pairs (same rays/segments arrays)."""
         if n >= self.n_pairs:
@@ -403,7 +408,8 @@ def _random_walk(rng, roots, start_dir, n_steps, step, max_turn_deg):
     return pts
 
 
-def hair_patch(seed: int = 3374, n_side: int = 100, n_seg: int = 10, thin: bool = False):
+def hair_patch(seed: int = 3374, n_side: int = 100, n_seg: int = 10, thin: bool = False,
+               device=None):
     """10,000 strands x 10 C1 cubic segments over the unit xz-square."""
     rng = _rng(seed)
     g = (np.arange(n_side) + 0.5) / n_side
@@ -421,7 +427,7 @@ def hair_patch(seed: int = 3374, n_side: int = 100, n_seg: int = 10, thin: bool 
         k = np.tile(np.arange(n_seg), S).astype(np.float64)
         s = (k[:, None] + np.array([0, 1 / 3, 2 / 3, 1])[None]) / n_seg
         radii = 4e-3 + (1e-3 - 4e-3) * s
-    return _validate(segs, radii)
+    return _validate(segs, radii, device)
 
 
 def fur_ball(seed: int = 3376, n_strands: int = 524288, n_seg: int = 4, device=None):
@@ -472,11 +478,13 @@ def _targets_on_segments(rng, ctrl, radii, seg_idx, dirs, scale_lo, scale_hi):
     return C + (rr * (1 + xi))[:, None] * n
 
 
-def config3(seed: int = 3374, n_rays: int = 1 << 20, k: int = 16, depth: int = 9) -> Workload:
-    """C3: hair patch, 2^20 targeted rays x (target segment + 15 nearest) = 2^24 pairs, D=9."""
+def config3(seed: int = 3374, n_rays: int = 1 << 20, k: int = 16, depth: int = 9,
+            device=None) -> Workload:
+    """C3: hair patch, 2^20 targeted rays x (target segment + 15 nearest) = 2^24 pairs, D=9.
+    device: run the validity check there (torch float64; see thick_ok)."""
     from scipy.spatial import cKDTree
 
-    ctrl, radii = hair_patch(seed)
+    ctrl, radii = hair_patch(seed, device=device)
     rng = _rng(seed + 1)
     seg = rng.integers(0, ctrl.shape[0], n_rays)
     w = _sphere(rng, n_rays)
@@ -484,7 +492,7 @@ def config3(seed: int = 3374, n_rays: int = 1 << 20, k: int = 16, depth: int = 9
     orig = tgt - 2.0 * w
     rays = _pack_rays(orig, w)
     centers = 0.5 * (ctrl.min(1) + ctrl.max(1)).astype(np.float64)
-    _, nn = cKDTree(centers).query(tgt, k=k)
+    _, nn = cKDTree(centers).query(tgt, k=k, workers=-1)
     nn = np.asarray(nn)
     # make sure the target segment is among the candidates (replace the k-th if absent)
     has = (nn == seg[:, None]).any(1)
@@ -516,10 +524,10 @@ def candidate_rounds(w: Workload) -> Workload:
                     np.ascontiguousarray(w.pairs[order]), w.depth, dict(w.meta, order="rounds"))
 
 
-def config4(seed: int = 3375, n_rays: int = 1 << 24, depth: int = 22) -> Workload:
+def config4(seed: int = 3375, n_rays: int = 1 << 24, depth: int = 22, device=None) -> Workload:
     """C4: thin fibers (r = 1e-4 chord), one pair per ray, half grazing (xi in +-2e-3),
     half inside (xi in [-1, 0]); D = 22."""
-    ctrl, radii = hair_patch(seed - 1, thin=True)
+    ctrl, radii = hair_patch(seed - 1, thin=True, device=device)
     rng = _rng(seed)
     seg = rng.integers(0, ctrl.shape[0], n_rays)
     w = _sphere(rng, n_rays)
