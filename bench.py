@@ -483,9 +483,9 @@ def run_c5(args, fx, dev, world, rank, peak):
     owned = perm[a:b]
     t_gen = time.perf_counter()
     w = gen.config5(n_rays=n_rays, ray_ids=owned, device=dev)
-    pairs, bounds, blocks = fxd.chunk_by_ray(w.pairs, owned, n_rays, K, device=dev)
+    pairs, bounds, blocks = fxd.chunk_by_ray(w.pairs, owned, n_rays, K, device=dev, local=True)
     t_gen = time.perf_counter() - t_gen
-    rays = torch.from_numpy(w.rays).to(dev)
+    rays = torch.from_numpy(w.rays[owned]).to(dev)  # this rank's rays only, in shard order
     segs = fx.build_segments(torch.from_numpy(w.ctrl).to(dev), torch.from_numpy(w.radii).to(dev))
     sn = fxd.ShardedNearest(fx, rays, segs, pairs, bounds, blocks, w.depth, dev)
     for _ in range(max(args.warmup, 1)):
@@ -525,7 +525,7 @@ def run_c5(args, fx, dev, world, rank, peak):
     if rank == 0 and world == 1:
         rng = np.random.default_rng(19)
         sub = np.sort(rng.choice(pairs.shape[0], 2048, replace=False))
-        wp = gen.Workload(w.name, w.rays, w.ctrl, w.radii, pairs[sub], w.depth)
+        wp = gen.Workload(w.name, w.rays[owned], w.ctrl, w.radii, pairs[sub], w.depth)
         sample = (wp, fx.unpack(sn.hits[torch.from_numpy(sub).to(dev)]))
     return res, sample
 

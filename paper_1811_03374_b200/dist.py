@@ -78,11 +78,14 @@ def timed_gather(local: torch.Tensor, iters: int = 3) -> float:
 
 
 def chunk_by_ray(pairs: np.ndarray, owned: np.ndarray, n_rays: int, n_chunks: int,
-                 device=None):
+                 device=None, local: bool = False):
     """Split a rank's pairs into n_chunks launches by blocks of its owned rays (shard order):
     chunk k holds every pair of owned[k m / K : (k+1) m / K], in the input's order within the
     chunk (so pairs sorted by segment stay so).  Returns (pairs reordered, chunk bounds [K+1],
-    owned ray blocks [K]).  device: sort there (torch)."""
+    ray blocks [K]).  local=True renumbers the rays by their position in `owned` (the rank then
+    keeps only rays[owned], its own rays contiguously, and chunk k reads the contiguous block
+    [k m / K, (k+1) m / K) of them): the pairs' ray column and the blocks are those positions.
+    device: sort there (torch)."""
     m = len(owned)
     pos = np.full(n_rays, -1, dtype=np.int64)
     pos[owned] = np.arange(m)
@@ -99,6 +102,12 @@ def chunk_by_ray(pairs: np.ndarray, owned: np.ndarray, n_rays: int, n_chunks: in
         order = np.argsort(ck, kind="stable")
     counts = np.bincount(ck, minlength=n_chunks)
     bounds = np.concatenate([[0], np.cumsum(counts)])
+    if local:
+        out = np.empty_like(pairs)
+        out[:, 0] = pp[order].astype(pairs.dtype)
+        out[:, 1] = pairs[order, 1]
+        blocks = [np.arange(k * m // n_chunks, (k + 1) * m // n_chunks) for k in range(n_chunks)]
+        return out, bounds, blocks
     blocks = [owned[k * m // n_chunks:(k + 1) * m // n_chunks] for k in range(n_chunks)]
     return np.ascontiguousarray(pairs[order]), bounds, blocks
 
@@ -108,9 +117,10 @@ class ShardedNearest:
     fiber_intersect_nearest (K2 + the per-ray nearest epilogue) on a compute stream, and per
     chunk -- as soon as its launch is done, on a second stream -- its per-ray records
     (fiber_nearest_records) gathered from every rank with one all_gather_into_tensor, so chunk k's
-    exchange overlaps chunk k+1's kernels.  No other data crosses ranks: rays and segments are
-    replicated, per-pair records stay on their GPU.  records[k] ends as [world x block_k, 4]
-    (rank-major), the rays of rank r's block k."""
+    exchange overlaps chunk k+1's kernels.  No other data crosses ranks: segments are
+    replicated, each rank holds its own rays (chunk_by_ray local=True: rays[owned], renumbered),
+    per-pair records stay on their GPU.  records[k] ends as [world x block_k, 4] (rank-major),
+    the rays of rank r's block k."""
 
     def __init__(self, fx, rays, segs, pairs: np.ndarray, bounds, blocks, depth: int, device):
         self.fx, self.rays, self.segs, self.depth = fx, rays, segs, depth
@@ -161,11 +171,14 @@ class ShardedNearest:
         cur.wait_stream(self.compute)
         cur.wait_stream(self.comm)
 
-    def records_by_ray(self, n_rays: int, all_blocks) -> torch.Tensor:
-        """The gathered records scattered to ray order: all_blocks[r][k] = rank r's block k."""
+    def records_by_ray(self, n_rays: int, all_owned) -> torch.Tensor:
+        """The gathered records scattered to global ray order: all_owned[r] = rank r's rays in
+        shard order (its local numbering)."""
         out = torch.full((n_rays, 4), float("nan"), dtype=torch.float32, device=self.out[0].device)
-        for k in range(len(self.blocks)):
-            ids = torch.cat([torch.as_tensor(np.asarray(all_blocks[r][k]), dtype=torch.int64)
-                             for r in range(self.world)]).to(out.device)
+        K = len(self.blocks)
+        for k in range(K):
+            ids = torch.cat([torch.as_tensor(np.asarray(
+                all_owned[r][k * len(all_owned[r]) // K:(k + 1) * len(all_owned[r]) // K]),
+                dtype=torch.int64) for r in range(self.world)]).to(out.device)
             out[ids] = self.out[k]
         return out

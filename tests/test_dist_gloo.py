@@ -127,3 +127,11 @@ def test_chunk_by_ray_partitions_the_shard():
                     key = ck[:, 1].astype(np.int64) << 32 | ck[:, 0].astype(np.int64)
                     assert np.all(np.diff(key) >= 0)
                 assert sorted(map(tuple, cp.tolist())) == sorted(map(tuple, local.tolist()))
+                # local numbering: the same pairs with rays renumbered by shard position, and
+                # chunk k's rays the contiguous positions of block k
+                lp, lb, lblocks = fxd.chunk_by_ray(local, owned, n, K, local=True)
+                assert np.array_equal(lb, bounds)
+                assert np.array_equal(owned[lp[:, 0].astype(np.int64)], cp[:, 0])
+                assert np.array_equal(lp[:, 1], cp[:, 1])
+                for k in range(K):
+                    assert np.array_equal(owned[lblocks[k]], blocks[k])

@@ -33,26 +33,22 @@ def _run(world, rank, out_dir):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     perm = fxd.ray_permutation(N_RAYS, seed=5)
-    blocks_all = []
-    for r in range(world):
-        a, b = fxd.shard_bounds(N_RAYS, world, r)
-        owned_r = perm[a:b]
-        m = len(owned_r)
-        blocks_all.append([owned_r[k * m // K:(k + 1) * m // K] for k in range(K)])
-    a, b = fxd.shard_bounds(N_RAYS, world, rank)
-    owned = perm[a:b]
+    all_owned = [perm[slice(*fxd.shard_bounds(N_RAYS, world, r))] for r in range(world)]
+    owned = all_owned[rank]
     w = gen.config5(n_rays=N_RAYS, n_strands=N_STRANDS, depth=DEPTH, ray_ids=owned)
-    pairs, bounds, blocks = fxd.chunk_by_ray(w.pairs, owned, N_RAYS, K)
-    rays = torch.from_numpy(w.rays).to(dev)
+    pairs, bounds, blocks = fxd.chunk_by_ray(w.pairs, owned, N_RAYS, K, local=True)
+    rays = torch.from_numpy(w.rays[owned]).to(dev)  # the rank's own rays, in shard order
     segs = fx.build_segments(torch.from_numpy(w.ctrl).to(dev), torch.from_numpy(w.radii).to(dev))
     sn = fxd.ShardedNearest(fx, rays, segs, pairs, bounds, blocks, DEPTH, dev)
     sn.step()
     sn.step()  # a second pass gives the same records (nearest is re-initialised)
     torch.cuda.synchronize()
-    rec = sn.records_by_ray(N_RAYS, blocks_all).cpu().numpy()
+    rec = sn.records_by_ray(N_RAYS, all_owned).cpu().numpy()
     np.save(os.path.join(out_dir, f"rec_{world}_{rank}.npy"), rec)
     np.save(os.path.join(out_dir, f"hits_{world}_{rank}.npy"), sn.hits.cpu().numpy())
-    np.save(os.path.join(out_dir, f"pairs_{world}_{rank}.npy"), pairs)
+    gp = pairs.copy()
+    gp[:, 0] = owned[pairs[:, 0].astype(np.int64)]  # back to global ray ids
+    np.save(os.path.join(out_dir, f"pairs_{world}_{rank}.npy"), gp)
 
 
 def _worker(rank, world, port, out_dir):
