@@ -15,6 +15,25 @@
 
 namespace fiberx {
 
+// Bounds checks of the checking build (-DFIBER_CHECKS, `python -m paper_1811_03374_b200.build
+// --variants` -> libfiber_checks.so): every index the kernels form is tested and a violation
+// traps with its location.  compute-sanitizer is closed on this GPU pool, so the GPU suite is
+// run against this build instead (scripts/run_checks.sh).  The product build compiles them out.
+#ifdef FIBER_CHECKS
+#define FIBER_CHECK(cond)                                                                  \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("FIBER_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,    \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                 \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define FIBER_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------------------------
 // small FP32 vector helpers (float4 = (x, y, z, w); w is the radius component)
 // ------------------------------------------------------------------------------------

@@ -166,6 +166,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
   const int64_t nleaf = (int64_t)1 << depth;
   const double inv = ldexp(1.0, -depth);
   int64_t k = (int64_t)(start >> (FIBER_MAX_DEPTH - depth));
+  FIBER_CHECK(depth >= 0 && depth <= FIBER_MAX_DEPTH && k >= 0 && k < nleaf);
   double t = (double)t32, u = 0.0;
   D4 n;
   if (kind == FIBER_KIND_CAP0 || kind == FIBER_KIND_CAP1) {
@@ -231,6 +232,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
           if (k + step < 0 || k + step >= nleaf) break;
           if (!test(k + step, qn, tn, ln, latn) || !(tn < ts)) break;
           k += step;
+          FIBER_CHECK(k >= 0 && k < nleaf);
         } else {
           // the FP32 leaf is off (below the crop level): walk towards the cylinder entry
           double c0;
@@ -242,6 +244,7 @@ __device__ __forceinline__ void finalize(const float4 ray0, const float4 ray1, c
           if (step == 0) break;
           dir = step;
           k += step;
+          FIBER_CHECK(k >= 0 && k < nleaf);
           ok = test(k, qn, tn, ln, latn);
           if (!ok) {  // keep walking from the new leaf's geometry
             q = qn;
@@ -398,6 +401,8 @@ constexpr int kWalk = 48;                  // K3's neighbour-leaf walk range
 
 __device__ __forceinline__ void write_record(const Params& p, uint32_t i, uint32_t ray, float t,
                                              float u, uint32_t n_oct, uint32_t flags) {
+  FIBER_CHECK(i < p.n_pairs);
+  FIBER_CHECK(!(p.nearest && (flags & FIBER_HIT)) || (int64_t)ray < p.n_rays);
   if (p.hits) p.hits[i] = make_float4(t, u, __uint_as_float(n_oct), __uint_as_float(flags));
   if (p.nearest && (flags & FIBER_HIT)) {
     const uint32_t low = (p.closest & 2) ? __ldg(&p.pairs[i]).y : i;
@@ -446,6 +451,7 @@ struct HodoRef {
   uint32_t* rs;  // FP64 resume point (start | log2(size) << 24), written at the first tie
   float4* wr;    // the pair's ray direction (xyz) and ray index (w bits), written at setup
   __device__ __forceinline__ void push(const Delta& f, float4 ival, uint32_t slot) const {
+    FIBER_CHECK(slot < (uint32_t)kFarCache);
     float4* q = far + slot * kRingF4 * kThreads;
     q[0] = f.p;
     q[kThreads] = f.d;
@@ -454,6 +460,7 @@ struct HodoRef {
     q[4 * kThreads] = ival;
   }
   __device__ __forceinline__ void pop(Delta& f, float4& ival, uint32_t slot) const {
+    FIBER_CHECK(slot < (uint32_t)kFarCache);
     const float4* q = far + slot * kRingF4 * kThreads;
     f.p = q[0];
     f.d = q[kThreads];
@@ -510,7 +517,9 @@ __device__ __forceinline__ bool prepare(const Params& p, uint32_t i, const uint2
     // a non-unit direction: the whole traversal runs in FP64 (K3), from the root
     p.hits[i] = make_float4(__uint_as_float((uint32_t)FIBER_MAX_DEPTH << 24), 0.0f, 0.0f,
                             __uint_as_float(e.badseg | kUncertain));
-    p.list_exact[atomicAdd(&p.counter[4], 1u)] = i;
+    const uint32_t k = atomicAdd(&p.counter[4], 1u);
+    FIBER_CHECK(k < p.n_pairs && i < p.n_pairs);
+    p.list_exact[k] = i;
     return false;
   }
   const float4 w = S.wh;
@@ -740,7 +749,8 @@ __device__ __forceinline__ void backtrack(Lane& L, HodoRef hs) {
   }
 }
 
-__device__ __forceinline__ void list_append(uint32_t* list, uint32_t k, uint32_t i, const Params&) {
+__device__ __forceinline__ void list_append(uint32_t* list, uint32_t k, uint32_t i, const Params& p) {
+  FIBER_CHECK(k < p.n_pairs && i < p.n_pairs);
   list[k] = i;
 }
 
@@ -837,8 +847,10 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
 
 // a7 for one provisional hit (all lanes of the batch run it together, converged).
 __device__ __noinline__ void finalize_one(const Params& p, uint32_t i) {
+  FIBER_CHECK(i < p.n_pairs);
   const float4 rec = p.hits[i];
   const uint2 pr = __ldg(&p.pairs[i]);
+  FIBER_CHECK((int64_t)pr.x < p.n_rays && (int64_t)pr.y < p.n_segs);
   const float4 ray0 = __ldg(&p.rays[2 * (int64_t)pr.x]);
   const float4 ray1 = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
   const float4 P0 = __ldg(&p.p0[pr.y]), P1 = __ldg(&p.p1[pr.y]);
@@ -953,6 +965,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
       }
       if (!active) {
         const uint32_t i = base + r;
+        FIBER_CHECK(base <= p.n_pairs);
         if (i < p.n_pairs) {
           const uint2 pr = __ldg(&p.pairs[i]);
           Prepared e;
@@ -1046,7 +1059,9 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
 #ifndef FIBER_NO_EXACT
   for (uint32_t k = gw + W * lane; k < n_exact; k += W * 32u) {
+    FIBER_CHECK(k < p.n_pairs);
     const uint32_t i = p.list_exact[k];
+    FIBER_CHECK(i < p.n_pairs);
     exact_one(p, i);  // the FP64 traversal, then the finalisation if it hit
     if (__float_as_uint(p.hits[i].w) & kProvisional) finalize_one(p, i);
   }
@@ -1055,7 +1070,10 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   // 32 provisional hits per warp, chunks dealt from the last warp down so the warps that
   // hold re-runs get them last
   for (uint32_t c = W - 1u - gw; c * 32u < n_fin; c += W)
-    if (c * 32u + lane < n_fin) finalize_one(p, p.list_fin[c * 32u + lane]);
+    if (c * 32u + lane < n_fin) {
+      FIBER_CHECK(c * 32u + lane < p.n_pairs && p.list_fin[c * 32u + lane] < p.n_pairs);
+      finalize_one(p, p.list_fin[c * 32u + lane]);
+    }
 #endif
 }
 
