@@ -990,10 +990,11 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
 #else
         const int st = step(L, hs, min_size);  // a3-a4
 #endif
-        if (st == ST_NEED_BT) {
-          backtrack(L, hs);  // a5
-        } else if (st != ST_RUNNING) {
-          ended = st;  // a6-a7 at the next refill (or the exit)
+        if (st == ST_NEED_BT) backtrack(L, hs);  // a5
+        // a pair ends at its leaf or miss -- or at its first near-tie decision: K3 re-runs
+        // it in FP64 from that node on, so the rest of its FP32 traversal would be discarded
+        if ((st != ST_RUNNING && st != ST_NEED_BT) || L.tie != 0u) {
+          ended = st == ST_HIT ? ST_HIT : ST_MISS;  // a6-a7 at the next refill (or the exit)
           active = false;
         }
       }
