@@ -279,9 +279,6 @@ int fiber_intersect_ex(const fiber_ray *rays, int64_t n_rays, const fiber_segmen
  *   out    device fiber_hit[n] (worst case): out[k] = hits[idx[k]], k < *count
  *   idx    device uint32[n] or NULL: idx[k] = the pair index of the k-th hit, increasing
  *   count  device uint32[1]: the number of records with FIBER_HIT
- * out, idx and count may be device memory or pinned host memory (cudaHostAlloc /
- * cudaMallocHost: device-accessible at the same address under unified addressing): the
- * kernels then write the results across PCIe as they produce them, with no copy to enqueue.
  * Deterministic (the k-th hit in pair order goes to slot k).  Scratch comes from the
  * library's stream-ordered pool.  Asynchronous like fiber_intersect.
  * Errors: FIBER_EINVAL (n out of range, count NULL, hits/out NULL with n > 0),

@@ -124,16 +124,12 @@ def _on(stream):
     return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
-def _hits(hits, n: int, device, name="hits", host_ok=False):
-    """A caller-supplied record buffer must hold n float32 [4] records on `device` (or, where
-    host_ok, in pinned host memory, which the device writes through unified addressing)."""
+def _hits(hits, n: int, device, name="hits"):
+    """A caller-supplied record buffer must hold n float32 [4] records on `device`."""
     if hits is None:
         return None
-    on_dev = isinstance(hits, torch.Tensor) and hits.is_cuda and hits.device == device
-    pinned = host_ok and isinstance(hits, torch.Tensor) and not hits.is_cuda and hits.is_pinned()
-    if not (on_dev or pinned):
-        raise FiberError(f"{name} must be a CUDA tensor on {device}"
-                         + (" or pinned host memory" if host_ok else ""))
+    if not (isinstance(hits, torch.Tensor) and hits.is_cuda and hits.device == device):
+        raise FiberError(f"{name} must be a CUDA tensor on {device}")
     if hits.dtype != torch.float32 or hits.dim() != 2 or hits.shape[1] != 4 or hits.shape[0] < n:
         raise FiberError(f"{name} must be float32 [n_pairs >= {n}, 4], got {hits.dtype} "
                          f"{tuple(hits.shape)}")
@@ -419,8 +415,7 @@ def intersect_closest(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, d
 def compact_hits(hits: torch.Tensor, out: torch.Tensor | None = None,
                  idx: torch.Tensor | None = None, count: torch.Tensor | None = None,
                  with_idx: bool = True, stream=None):
-    """fiber_compact_hits: (out f32[n,4], idx i32[n] or None, count i32[1]) on the device or in
-    pinned host memory (the kernels then write the results across PCIe directly);
+    """fiber_compact_hits: (out f32[n,4], idx i32[n] or None, count i32[1]) on the device;
     out[:count] are the records with FIBER_HIT in pair order, idx[:count] their pair indices."""
     with _on(stream):
         hits = _dev(hits, torch.float32, (4,), "hits")
@@ -431,18 +426,12 @@ def compact_hits(hits: torch.Tensor, out: torch.Tensor | None = None,
             idx = torch.empty((n,), dtype=torch.int32, device=hits.device)
         if count is None:
             count = torch.empty((1,), dtype=torch.int32, device=hits.device)
-        _hits(out, n, hits.device, "out", host_ok=True)
-
-        def reachable(t):  # on the hits' device, or pinned host memory (unified addressing)
-            return (t.is_cuda and t.device == hits.device) or (not t.is_cuda and t.is_pinned())
-
+        _hits(out, n, hits.device, "out")
         if idx is not None and (idx.dtype != torch.int32 or idx.numel() < n or not idx.is_contiguous()
-                                or not reachable(idx)):
-            raise FiberError("compact_hits: idx must be a contiguous int32[>= n] on the hits' "
-                             "device or in pinned host memory")
-        if count.dtype != torch.int32 or count.numel() < 1 or not reachable(count):
-            raise FiberError("compact_hits: count must be int32[1] on the hits' device or in "
-                             "pinned host memory")
+                                or idx.device != hits.device):
+            raise FiberError("compact_hits: idx must be a contiguous int32[>= n] on the hits' device")
+        if count.dtype != torch.int32 or count.numel() < 1 or count.device != hits.device:
+            raise FiberError("compact_hits: count must be int32[1] on the hits' device")
         _check(lib().fiber_compact_hits(hits.data_ptr(), n, out.data_ptr(),
                                         idx.data_ptr() if idx is not None else None,
                                         count.data_ptr(), _stream(stream)), "fiber_compact_hits")

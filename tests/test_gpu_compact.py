@@ -83,26 +83,3 @@ def test_compact_real_records_and_without_idx(fx):
     # the compacted t values are the hits' (finite, before t_max), the misses' are not copied
     t = out[:k, 0].cpu().numpy()
     assert np.isfinite(t).all()
-
-
-def test_compact_into_pinned_host_memory(fx):
-    """out / idx / count in pinned host memory (written across PCIe by the kernels, unified
-    addressing) equal the device-memory results."""
-    import torch
-
-    w = gen.config2("A", n_rays=1 << 16, depth=9)
-    rays, segs, pairs = fx.to_device(w)
-    hits = fx.intersect(rays, segs, pairs, 9)
-    out_d, idx_d, cnt_d = fx.compact_hits(hits)
-    n = hits.shape[0]
-    out_h = torch.empty((n, 4), dtype=torch.float32).pin_memory()
-    idx_h = torch.empty((n,), dtype=torch.int32).pin_memory()
-    cnt_h = torch.zeros((1,), dtype=torch.int32).pin_memory()
-    fx.compact_hits(hits, out=out_h, idx=idx_h, count=cnt_h)
-    torch.cuda.synchronize()
-    k = int(cnt_d.item())
-    assert int(cnt_h[0]) == k > 1000
-    assert torch.equal(out_h[:k].view(torch.int32), out_d[:k].cpu().view(torch.int32))
-    assert torch.equal(idx_h[:k], idx_d[:k].cpu())
-    with pytest.raises(fx.FiberError):  # pageable host memory is not device-accessible
-        fx.compact_hits(hits, out=torch.empty((n, 4)), idx=idx_h, count=cnt_h)
