@@ -947,18 +947,17 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
   while (true) {
     const unsigned idle = __ballot_sync(0xffffffffu, !active);
     if (!drained && (__popc(idle) >= (int)kRefill || idle == 0xffffffffu)) {
+      // the claim first: its atomic's latency overlaps the record writing below
+      const uint32_t k = __popc(idle), r = __popc(idle & lt);
+      unsigned long long claimed = 0;
+      if (lane == 0) claimed = atomicAdd(pair_counter, (unsigned long long)k);
       // a6-a7 for the lanes that finished since the last refill, together (the lane keeps
       // its state until then), so the record writer runs at the refill's SIMT width
       if (ended != ST_RUNNING) {
         end_pair(p, pair, L, ended, badseg, hs);
         ended = ST_RUNNING;
       }
-      const uint32_t k = __popc(idle), r = __popc(idle & lt);
-      uint32_t base = 0;
-      if (lane == 0) {
-        const unsigned long long b = atomicAdd(pair_counter, (unsigned long long)k);
-        base = (uint32_t)min(b, (unsigned long long)p.n_pairs);
-      }
+      uint32_t base = (uint32_t)min(claimed, (unsigned long long)p.n_pairs);
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base + k >= p.n_pairs) {
         drained = true;
