@@ -81,6 +81,7 @@ def parse():
     p.add_argument("--c5-rays", type=int, default=1 << 24)
     p.add_argument("--c5-chunks", type=int, default=8)
     p.add_argument("--depths", type=str, default=None, help="e.g. 2-22 or 4,9,22 (C2 sweep)")
+    p.add_argument("--streams", type=int, default=3, help="streams the C2 step's launches use")
     return p.parse_args()
 
 
@@ -390,7 +391,8 @@ def run_ours(args):
     t0 = time.perf_counter()
     with ClockSampler(local) as clk:
         step_ms = time_steps_pipelined(fx, data, launches, args.steps, args.warmup, flush,
-                                       [hits, torch.empty_like(hits)])
+                                       [hits] + [torch.empty_like(hits)
+                                                 for _ in range(args.streams - 1)])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -434,7 +436,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "value_serialized": round(world * pairs_per_step * args.steps / (ser_ms * 1e-3) / 1e9, 4),
-        "value_note": "value: whole steps, the 63 launches issued back to back on 2 streams (L2 "
+        "value_note": f"value: whole steps, the 63 launches issued back to back on {args.streams} streams (L2 "
                       "flushed before each step); value_serialized: the sum of the launches timed "
                       "one by one, L2 flushed before each (by_depth and the roofline use these)",
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",

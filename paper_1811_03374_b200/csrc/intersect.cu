@@ -1058,7 +1058,7 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   const uint32_t W = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
 #ifndef FIBER_NO_EXACT
-  for (uint32_t k = gw + W * lane; k < n_exact; k += W * 32u) {
+  for (uint64_t k = gw + (uint64_t)W * lane; k < n_exact; k += (uint64_t)W * 32u) {
     FIBER_CHECK(k < p.n_pairs);
     const uint32_t i = p.list_exact[k];
     FIBER_CHECK(i < p.n_pairs);
@@ -1069,7 +1069,7 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
 #ifndef FIBER_NO_FIN
   // 32 provisional hits per warp, chunks dealt from the last warp down so the warps that
   // hold re-runs get them last
-  for (uint32_t c = W - 1u - gw; c * 32u < n_fin; c += W)
+  for (uint64_t c = W - 1u - gw; c * 32u < n_fin; c += W)
     if (c * 32u + lane < n_fin) {
       FIBER_CHECK(c * 32u + lane < p.n_pairs && p.list_fin[c * 32u + lane] < p.n_pairs);
       finalize_one(p, p.list_fin[c * 32u + lane]);

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.parity import assert_parity, compare
+from tests.parity import TOL_T, assert_parity, compare
 from workloads import gen
 
 pytestmark = pytest.mark.gpu
@@ -209,3 +209,51 @@ def test_ragged_sizes_and_extreme_depths(fx, n_rays, depth):
     w = gen.config2("B", n_rays=n_rays, depth=depth, targeted=True)
     rep = compare(_run(fx, w), _oracle(w))
     assert_parity(rep)
+
+
+def test_full_size_config5_sharded_sampled(fx):
+    """C5 at its BASELINE size (2^24 fur rays x 16 candidates = 2^28 pairs, D = 6) in the
+    launch configuration bench.py times (dist.ShardedNearest at one rank: 8 chunk launches of
+    the nearest epilogue, per-ray records from fiber_nearest_records): 2,048 sampled pairs'
+    records and 256 sampled rays' nearest-hit records against the oracle."""
+    import torch
+
+    from paper_1811_03374_b200 import dist as fxd
+
+    dev = torch.device("cuda", 0)
+    n_rays = 1 << 24
+    owned = fxd.ray_permutation(n_rays, seed=5)
+    w = gen.config5(n_rays=n_rays, ray_ids=owned, device=dev)
+    pairs, bounds, blocks = fxd.chunk_by_ray(w.pairs, owned, n_rays, 8, device=dev, local=True)
+    rays_l = w.rays[owned]
+    segs = fx.build_segments(torch.from_numpy(w.ctrl).to(dev), torch.from_numpy(w.radii).to(dev))
+    sn = fxd.ShardedNearest(fx, torch.from_numpy(rays_l).to(dev), segs, pairs, bounds, blocks, 6, dev)
+    sn.step()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(53)
+    sub = np.sort(rng.choice(pairs.shape[0], 2048, replace=False))
+    g = fx.unpack(sn.hits[torch.from_numpy(sub).to(dev)])
+    o = oracle.intersect(rays_l, w.ctrl, w.radii, pairs[sub], 6)
+    assert_parity(compare(g, o))
+    # per-ray records: rays of chunk 0 (local ids 0 .. m/8), each against all its candidates
+    rec = torch.cat(sn.out).cpu().numpy()  # chunk-major, rank-major inside (one rank)
+    ids = np.sort(rng.choice(len(blocks[0]), 256, replace=False))
+    cand = pairs[pairs[:, 0] < len(blocks[0])]
+    checked = 0
+    for r in ids:
+        pr = cand[cand[:, 0] == r]
+        oo = oracle.intersect(rays_l, w.ctrl, w.radii, pr, 6)
+        got = rec[r]
+        if not oo["hit"].any():
+            assert np.isinf(got[0]) and got.view(np.uint32)[3] == 0xFFFFFFFF
+            continue
+        if oo["grazing"].any():
+            continue
+        ts = np.where(oo["hit"], oo["t"], np.inf)
+        j = int(np.argmin(ts))
+        second = np.sort(ts)[1] if oo["hit"].sum() > 1 else np.inf
+        assert abs(got[0] - ts[j]) <= TOL_T * ts[j]
+        if second - ts[j] > 2 * TOL_T * ts[j]:  # a unique winner: its segment
+            assert got.view(np.uint32)[3] == pr[j, 1]
+        checked += 1
+    assert checked > 50
