@@ -229,11 +229,12 @@ int fiber_grid_closest(const fiber_grid *grid, const fiber_ray *rays, int64_t n_
  * segment pair.seg at subdivision depth max_depth and write hits[i].
  *   rays      device fiber_ray[n_rays]
  *   segs      built by fiber_build_segments (host descriptor, device planes)
- *   pairs     device fiber_pair[n_pairs]; indices out of range give FIBER_BAD_INPUT
+ *   pairs     device fiber_pair[n_pairs], 0 <= n_pairs < 2^31 (a larger set takes several
+ *             calls); indices out of range give FIBER_BAD_INPUT
  *   max_depth D in [0, 23]: the number of halvings of [0, 1]; min_size = 2^(23 - D)
  *   hits      device fiber_hit[n_pairs]
  * Results are bit-identical for the same inputs regardless of launch shape or order.
- * Errors: FIBER_EINVAL, FIBER_EDEVICE, FIBER_ECUDA. */
+ * Errors: FIBER_EINVAL (also n_pairs >= 2^31, n_rays >= 2^32), FIBER_EDEVICE, FIBER_ECUDA. */
 int fiber_intersect(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
                     const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
                     void *cuda_stream);

@@ -1058,7 +1058,9 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
   const uint32_t W = gridDim.x * (blockDim.x >> 5);
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
 #ifndef FIBER_NO_EXACT
-  for (uint64_t k = gw + (uint64_t)W * lane; k < n_exact; k += (uint64_t)W * 32u) {
+  // 32-bit indices (64-bit ones made this loop 3x slower on C4): n_pairs < 2^31 (fiber.h) and
+  // W * 32 < 2^17, so k never wraps
+  for (uint32_t k = gw + W * lane; k < n_exact; k += W * 32u) {
     FIBER_CHECK(k < p.n_pairs);
     const uint32_t i = p.list_exact[k];
     FIBER_CHECK(i < p.n_pairs);
@@ -1069,7 +1071,7 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
 #ifndef FIBER_NO_FIN
   // 32 provisional hits per warp, chunks dealt from the last warp down so the warps that
   // hold re-runs get them last
-  for (uint64_t c = W - 1u - gw; c * 32u < n_fin; c += W)
+  for (uint32_t c = W - 1u - gw; c * 32u < n_fin; c += W)
     if (c * 32u + lane < n_fin) {
       FIBER_CHECK(c * 32u + lane < p.n_pairs && p.list_fin[c * 32u + lane] < p.n_pairs);
       finalize_one(p, p.list_fin[c * 32u + lane]);
@@ -1149,7 +1151,7 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
                             fiber_hit* hits, uint64_t* nearest, void* event_after_traverse,
                             void* stream, int closest = 0) {
   if (n_rays < 0 || n_pairs < 0 || n_rays >= ((int64_t)1 << 32) ||
-      n_pairs >= ((int64_t)1 << 32) - 64 || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
+      n_pairs >= ((int64_t)1 << 31) || max_depth < 0 || max_depth > FIBER_MAX_DEPTH || !segs)
     return set_error(FIBER_EINVAL, "fiber_intersect: bad size or depth");
   if (n_pairs > 0 && (!rays || !pairs || (!hits && !nearest) || !segs->p0 || !segs->p1 ||
                       !segs->p2 || !segs->p3 || !segs->flags))

@@ -146,3 +146,13 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 s = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in s and "from oracle" not in s and "oracle.c" not in s, f
+
+
+def test_intersect_pair_count_limit():
+    """n_pairs >= 2^31 is rejected before anything is enqueued (fiber.h: the K3 list loops
+    index with 32 bits)."""
+    from paper_1811_03374_b200 import fiber
+
+    L = fiber.lib()
+    segs = fiber._Segs(1, 1, 1, 1, 1, 1)
+    assert L.fiber_intersect(1, 1, ctypes.byref(segs), 1, 1 << 31, 4, 1, None) == -1
