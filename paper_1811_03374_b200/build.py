@@ -51,5 +51,4 @@ if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     if "--variants" in sys.argv:  # test builds (IEEE-rounded FP32 math)
         build(force=True, out=os.path.join(HERE, "libfiber_ieee.so"), defines=("FIBER_IEEE_MATH",))
-        build(force=True, out=os.path.join(HERE, "libfiber_trace.so"), defines=("FIBER_TRACE",))
         build(force=True, out=os.path.join(HERE, "libfiber_checks.so"), defines=("FIBER_CHECKS",))

@@ -30,11 +30,7 @@ constexpr int kThreads = FIBER_K2_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kFarCache = FIBER_FAR_CACHE;  // per-lane cache of pending far children
 constexpr int kRingF4 = 5;  // a ring entry: the parent's Delta (4 float4) + its interval
-#ifndef FIBER_NO_RAYSTASH
 constexpr int kRayStash = 1;  // per-lane copy of the ray direction + ray index (end_pair)
-#else
-constexpr int kRayStash = 0;
-#endif
 constexpr size_t kSmemBytes = (size_t)(4 + kRingF4 * kFarCache + kRayStash) * kThreads * sizeof(float4) +
                                kThreads * sizeof(uint32_t);  // + the lanes' FP64 resume points
 
@@ -382,15 +378,7 @@ struct Params {
                           // counter (64-bit), [4]/[5] list appends = list lengths for K3
   uint32_t* list_exact;   // pairs K2 flagged for the FP64 re-run   [n_pairs]
   uint32_t* list_fin;     // provisional hits for the FP64 finalise [n_pairs]
-#ifdef FIBER_TRACE
-  uint32_t trace_pair;  // test build only: per-iteration records of one pair
-  float4* trace;        // [kTraceCap] x 3 float4
-#endif
 };
-#ifdef FIBER_TRACE
-constexpr int kTraceCap = 256;
-__device__ unsigned int g_trace_n;
-#endif
 
 // Internal flags of records between the kernels (never visible after fiber_intersect
 // returns): a provisional hit, and a pair to re-run in FP64; K3 consumes both.
@@ -587,8 +575,7 @@ __device__ __forceinline__ void note_tie(Lane& L, HodoRef hs, uint32_t t) {
 
 // One iteration: node test, then descend.  Returns ST_RUNNING, ST_MISS, ST_HIT (leaf
 // accepted; L.c0 holds the cylinder entry) or ST_NEED_BT (pruned with levels pending).
-__device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
-                                    float4* trace = nullptr) {
+__device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size) {
   ++L.tests;
   float c0, c1, tie_e, inv_sin;
   const bool cyl = cylinder(L.cur, c0, c1, &tie_e, &inv_sin, L.delta);
@@ -601,17 +588,6 @@ __device__ __forceinline__ int step(Lane& L, HodoRef hs, uint32_t min_size,
   note_tie(L, hs, (tie_e < 0.0f ? 1u : 0u) |
                   ((cyl && ((fabsf(c1 - L.tmin) < tb) | (fabsf(L.tmax - c0) < tb) |
                             (fabsf(L.tmax - L.tmin) < 2.0f * L.terr))) ? 2u : 0u));
-#ifdef FIBER_TRACE
-  if (trace) {
-    unsigned k = atomicAdd(&g_trace_n, 1u);
-    if (k < kTraceCap) {
-      trace[3 * k] = make_float4(__uint_as_float(L.start), __uint_as_float(L.size),
-                                 __uint_as_float(L.bits), __uint_as_float(pass ? 1u : 0u));
-      trace[3 * k + 1] = make_float4(c0, c1, L.tmin, L.tmax);
-      trace[3 * k + 2] = make_float4(__uint_as_float(L.tag), __uint_as_float(L.ncache), 0.0f, 0.0f);
-    }
-  }
-#endif
   // a5 for a cached far child is folded into the descent below: jump_up to the deepest
   // pending level (the most recent push), then the far child of the cached parent is built
   // with the same split arithmetic as the near child was, and its interval is the parent's
@@ -788,13 +764,8 @@ __device__ __forceinline__ void end_pair(const Params& p, uint32_t i, const Lane
       // and the FP32 coordinate error is far below the radius (normal error ~ delta / r);
       // otherwise a provisional record for K3's FP64 re-solve
       if (!inside && p.depth <= FIBER_FP32_FIN_DEPTH && L.delta < 1.220703125e-4f * L.cur.p.w) {
-#ifndef FIBER_NO_RAYSTASH
         const float4 w = *hs.wr;  // stashed at setup: no dependent pair -> ray reload
         const uint2 pr = make_uint2(__float_as_uint(w.w), 0u);
-#else
-        const uint2 pr = __ldg(&p.pairs[i]);
-        const float4 w = __ldg(&p.rays[2 * (int64_t)pr.x + 1]);
-#endif
         const float4 wh = w;  // a unit direction (prepare), as frame32<true>
         float4 b1, b2;
         onb(wh, b1, b2);
@@ -984,11 +955,7 @@ __global__ void __launch_bounds__(kThreads, FIBER_K2_MINBLOCKS) intersect_kernel
 #pragma unroll 1
     for (int k = 0; k < kEpoch; ++k) {
       if (active) {
-#ifdef FIBER_TRACE
-        const int st = step(L, hs, min_size, pair == p.trace_pair ? p.trace : nullptr);
-#else
         const int st = step(L, hs, min_size);  // a3-a4
-#endif
         if (st == ST_NEED_BT) backtrack(L, hs);  // a5
         // a pair ends at its leaf or miss -- or at its first near-tie decision: K3 re-runs
         // it in FP64 from that node on, so the rest of its FP32 traversal would be discarded
@@ -1121,10 +1088,6 @@ static const LaunchInfo* launch_info() {
   return &info[dev];
 }
 
-#ifdef FIBER_TRACE
-static uint32_t g_trace_pair = 0xffffffffu;
-static float4* g_trace_buf = nullptr;
-#endif
 
 // The per-call scratch (two work lists of n_pairs entries, and records when the caller
 // gives none) comes from a private stream-ordered memory pool per device that keeps its
@@ -1198,10 +1161,6 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   p.n_pairs = (uint32_t)n_pairs;
   p.depth = max_depth;
   p.min_size = 1u << (FIBER_MAX_DEPTH - max_depth);
-#ifdef FIBER_TRACE
-  p.trace_pair = g_trace_pair;
-  p.trace = g_trace_buf;
-#endif
   p.hits = (float4*)hits;
   p.nearest = (unsigned long long*)nearest;
   p.closest = closest;
