@@ -600,7 +600,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                      torch.from_numpy(w.pairs.view(np.int32)).pin_memory(),
                      torch.from_numpy(w.ctrl).pin_memory(), torch.from_numpy(w.radii).pin_memory()))
     nb = len(host)
-    NC = 2  # compute streams
+    NC = 3  # compute streams
     d_in = [(torch.empty((n, 8), dtype=torch.float32, device=dev),
              torch.empty((n, 2), dtype=torch.int32, device=dev),
              torch.empty((1, 4, 3), dtype=torch.float32, device=dev),
@@ -710,7 +710,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
             "ms_per_step": round(ms / k, 3), "steps": k,
             "hits_per_step": int(counts["hits"]),
             "note": "results = per launch the hit records in pair order + their pair indices "
-                    "(fiber_compact_hits) + the count; launches alternate between 2 compute "
+                    "(fiber_compact_hits) + the count; launches alternate between 3 compute "
                     "streams, copies on two copy streams overlapping them (ring of 8 result slots)"}
 
 
