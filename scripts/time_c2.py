@@ -8,6 +8,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if "--lib" in sys.argv:  # a test build libfiber_VARIANT.so (the binding reads this at import)
+    os.environ["FIBER_LIB_VARIANT"] = sys.argv[sys.argv.index("--lib") + 1]
 import paper_1811_03374_b200 as fx  # noqa: E402
 from workloads import gen  # noqa: E402
 
@@ -32,6 +34,7 @@ def time_launch(w, depth, reps=5):
 
 def main():
     torch.cuda.set_device(0)
+    print(f"library {fx.fiber.LIB_PATH}", flush=True)
     for f in "ABC":
         w = gen.config2(f, n_rays=1 << 20, depth=22)
         row = []
