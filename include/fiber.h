@@ -239,11 +239,13 @@ int fiber_intersect(const fiber_ray *rays, int64_t n_rays, const fiber_segments 
                     const fiber_pair *pairs, int64_t n_pairs, int max_depth, fiber_hit *hits,
                     void *cuda_stream);
 
-/* fiber_intersect with the fused per-ray nearest-hit epilogue: in
- * addition (hits may be NULL), for every hit pair atomically
+/* fiber_intersect with the per-ray nearest-hit epilogue: in addition
+ * (hits may be NULL), for every hit pair atomically
  *   nearest[pair.ray] = min(nearest[pair.ray], (bits(t) << 32) | i)
  * where i is the pair index in this call.  `nearest` (device uint64[n_rays]) must be
- * initialised by the caller (fiber_nearest_init) before the first call of a batch. */
+ * initialised by the caller (fiber_nearest_init) before the first call of a batch.  The keys
+ * are formed by a pass over the finished records queued after the traversal on the same
+ * stream (the result is the same min as forming them at each hit). */
 int fiber_intersect_nearest(const fiber_ray *rays, int64_t n_rays, const fiber_segments *segs,
                             const fiber_pair *pairs, int64_t n_pairs, int max_depth,
                             fiber_hit *hits, uint64_t *nearest, void *cuda_stream);

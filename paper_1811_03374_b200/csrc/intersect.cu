@@ -1046,6 +1046,23 @@ __global__ void __launch_bounds__(kK3Threads, FIBER_K3_MINBLOCKS) finalize_kerne
 #endif
 }
 
+// K4, the per-ray nearest keys of fiber_intersect_nearest (no running bound): one pass over
+// the finished records, atomicMin((bits(t) << 32) | i) into nearest[ray] for every hit --
+// the same keys write_record would have formed.  Run after K3 instead of inside K2 because
+// K2's reductions there share the L2 atomic units with its pair-claim atomics and stall the
+// refills (C5 2.06 -> 3.02 ms per 2^25-pair chunk with them inline).
+__global__ void __launch_bounds__(256) nearest_kernel(const Params p, unsigned long long* nearest) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_pairs;
+       i += gridDim.x * blockDim.x) {
+    const float4 r = __ldcs(&p.hits[i]);
+    if (__float_as_uint(r.w) & FIBER_HIT) {
+      const uint32_t ray = __ldg(&p.pairs[i]).x;
+      FIBER_CHECK((int64_t)ray < p.n_rays);
+      atomicMin(&nearest[ray], ((unsigned long long)__float_as_uint(r.x) << 32) | i);
+    }
+  }
+}
+
 __global__ void fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1162,7 +1179,14 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
   p.depth = max_depth;
   p.min_size = 1u << (FIBER_MAX_DEPTH - max_depth);
   p.hits = (float4*)hits;
-  p.nearest = (unsigned long long*)nearest;
+  // fiber_intersect_nearest: the keys are formed by K4 after K3 (nearest_kernel), so K2 and
+  // K3 run as for fiber_intersect; with a running bound (closest) they need them at once
+#ifdef FIBER_NEAREST_INLINE  // test build: the keys inside K2/K3
+  const bool defer = false;
+#else
+  const bool defer = nearest && closest == 0;
+#endif
+  p.nearest = defer ? nullptr : (unsigned long long*)nearest;
   p.closest = closest;
   p.counter = counter;
   p.list_exact = (uint32_t*)((char*)scratch + kCounterBytes);
@@ -1193,6 +1217,12 @@ static int launch_intersect(const fiber_ray* rays, int64_t n_rays, const fiber_s
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, finalize_kernel, p);
     rc = check_launch("fiber_intersect (finalize)");
+  }
+  if (rc == FIBER_OK && defer) {
+    int64_t nblocks = (n_pairs + 255) / 256;
+    if (nblocks > (int64_t)li->sms * 8) nblocks = (int64_t)li->sms * 8;
+    nearest_kernel<<<(unsigned)nblocks, 256, 0, st>>>(p, (unsigned long long*)nearest);
+    rc = check_launch("fiber_intersect (nearest)");
   }
   cudaFreeAsync(scratch, st);
   return rc;
