@@ -616,6 +616,10 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
     main = torch.cuda.current_stream()
     comps = [torch.cuda.Stream(device=dev) for _ in range(NC)]
     up, down = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    # the 4-byte counts come back on their own stream: behind the bulk hit copies on `down`
+    # they would hold the host (which reads each count before it can size that launch's
+    # copy) and with it the launches it has yet to enqueue
+    cnt = torch.cuda.Stream(device=dev)
     ev_in = [torch.cuda.Event() for _ in range(nb)]
     ev_used = [[torch.cuda.Event() for _ in range(NC)] for _ in range(nb)]  # fiber f consumed
     ev_done = [torch.cuda.Event() for _ in range(R)]
@@ -629,6 +633,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
         ev_cnt[s].synchronize()  # this launch's count is on the host
         k = int(h_cnt[s])
         with torch.cuda.stream(down):
+            down.wait_event(ev_cnt[s])  # (the count's copy followed the launch)
             h_out[s][:k].copy_(d_out[s][:k], non_blocking=True)
             h_idx[s][:k].copy_(d_idx[s][:k], non_blocking=True)
             ev_free[s].record(down)
@@ -637,7 +642,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
 
     def step():
         counts["h2d"] = counts["d2h"] = counts["hits"] = 0
-        for c in comps + [up, down]:
+        for c in comps + [up, down, cnt]:
             c.wait_stream(main)
         with torch.cuda.stream(up):  # all uploads of the step, in order, on the copy stream
             for f, (r, p, c, ra) in enumerate(host):
@@ -669,10 +674,10 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                     fx.compact_hits(d_hits[j % NC], out=d_out[s], idx=d_idx[s],
                                     count=d_cnt[s:s + 1], stream=cs)
                     ev_done[s].record(cs)
-                with torch.cuda.stream(down):
-                    down.wait_event(ev_done[s])
+                with torch.cuda.stream(cnt):
+                    cnt.wait_event(ev_done[s])
                     h_cnt[s:s + 1].copy_(d_cnt[s:s + 1], non_blocking=True)
-                    ev_cnt[s].record(down)
+                    ev_cnt[s].record(cnt)
                 pending.append(s)
                 if len(pending) > LAG:
                     drain(pending.popleft())
@@ -681,7 +686,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                 e.record(c)
         while pending:
             drain(pending.popleft())
-        for c in comps + [down]:  # the step ends when its last hits are on the host
+        for c in comps + [down, cnt]:  # the step ends when its last hits are on the host
             main.wait_stream(c)
         return counts["h2d"], counts["d2h"]
 
