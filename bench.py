@@ -613,6 +613,9 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
     h_out = [torch.empty((n, 4), dtype=torch.float32).pin_memory() for _ in range(R)]
     h_idx = [torch.empty((n,), dtype=torch.int32).pin_memory() for _ in range(R)]
     h_cnt = torch.zeros((R,), dtype=torch.int32).pin_memory()
+    d_cnt_s = [d_cnt[i:i + 1] for i in range(R)]  # per-slot views, made once
+    h_cnt_s = [h_cnt[i:i + 1] for i in range(R)]
+    h_cnt_np = h_cnt.numpy()  # the same pinned memory, read without a tensor per access
     main = torch.cuda.current_stream()
     comps = [torch.cuda.Stream(device=dev) for _ in range(NC)]
     up, down = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -627,11 +630,13 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
     ev_free = [torch.cuda.Event() for _ in range(R)]
     for e in [x for row in ev_used for x in row] + ev_free:
         e.record(main)
-    counts = {"h2d": 0, "d2h": 0, "hits": 0}
+    counts = {"h2d": 0, "d2h": 0, "hits": 0, "wait_s": 0.0}
 
     def drain(s):
+        t0 = time.perf_counter()
         ev_cnt[s].synchronize()  # this launch's count is on the host
-        k = int(h_cnt[s])
+        counts["wait_s"] += time.perf_counter() - t0
+        k = int(h_cnt_np[s])
         with torch.cuda.stream(down):
             down.wait_event(ev_cnt[s])  # (the count's copy followed the launch)
             h_out[s][:k].copy_(d_out[s][:k], non_blocking=True)
@@ -642,6 +647,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
 
     def step():
         counts["h2d"] = counts["d2h"] = counts["hits"] = 0
+        counts["wait_s"] = 0.0
         for c in comps + [up, down, cnt]:
             c.wait_stream(main)
         with torch.cuda.stream(up):  # all uploads of the step, in order, on the copy stream
@@ -657,27 +663,28 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
         j = 0
         for f in range(nb):
             d_rays, d_pairs, d_ctrl, d_rad = d_in[f]
-            segs = None
+            segs, ev_seg, ready = None, torch.cuda.Event(), set()
             for D in depths:
-                s, cs = j % R, comps[j % NC]
-                with torch.cuda.stream(cs):
+                s, c = j % R, j % NC
+                cs = comps[c]
+                if c not in ready:  # once per fiber and stream: its inputs and segments
                     cs.wait_event(ev_in[f])
-                    if segs is None:
-                        segs = fx.build_segments(d_ctrl, d_rad, stream=cs)
-                        keep.append(segs)
-                        ev_seg = torch.cuda.Event()
-                        ev_seg.record(cs)
-                    else:
+                    if segs is not None:
                         cs.wait_event(ev_seg)
-                    cs.wait_event(ev_free[s])  # slot s's previous result is on the host
-                    fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits[j % NC], stream=cs)
-                    fx.compact_hits(d_hits[j % NC], out=d_out[s], idx=d_idx[s],
-                                    count=d_cnt[s:s + 1], stream=cs)
-                    ev_done[s].record(cs)
+                    ready.add(c)
+                if segs is None:
+                    segs = fx.build_segments(d_ctrl, d_rad, stream=cs)
+                    keep.append(segs)
+                    ev_seg.record(cs)
+                cs.wait_event(ev_free[s])  # slot s's previous result is on the host
+                fx.intersect(d_rays, segs, d_pairs, D, hits=d_hits[c], stream=cs)
+                fx.compact_hits(d_hits[c], out=d_out[s], idx=d_idx[s], count=d_cnt_s[s],
+                                stream=cs)
+                ev_done[s].record(cs)
+                cnt.wait_event(ev_done[s])
                 with torch.cuda.stream(cnt):
-                    cnt.wait_event(ev_done[s])
-                    h_cnt[s:s + 1].copy_(d_cnt[s:s + 1], non_blocking=True)
-                    ev_cnt[s].record(cnt)
+                    h_cnt_s[s].copy_(d_cnt_s[s], non_blocking=True)
+                ev_cnt[s].record(cnt)
                 pending.append(s)
                 if len(pending) > LAG:
                     drain(pending.popleft())
@@ -699,8 +706,12 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
     k = max(1, min(args.steps, 3))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
+    host_s = wait_s = 0.0
     for _ in range(k):
+        t0 = time.perf_counter()
         h2d, d2h = step()
+        host_s += time.perf_counter() - t0
+        wait_s += counts["wait_s"]
     e1.record(main)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -714,6 +725,10 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(ms / k, 3), "steps": k,
             "hits_per_step": int(counts["hits"]),
+            # host time in step() (enqueueing + waiting for counts) and the part spent waiting:
+            # a small wait share means the host's enqueueing, not the device, sets the pace
+            "host_ms_per_step": round(host_s * 1e3 / k, 3),
+            "host_wait_ms_per_step": round(wait_s * 1e3 / k, 3),
             "note": "results = per launch the hit records in pair order + their pair indices "
                     "(fiber_compact_hits) + the count; launches alternate between 3 compute "
                     "streams, copies on two copy streams overlapping them (ring of 8 result slots)"}

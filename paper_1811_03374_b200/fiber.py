@@ -124,6 +124,13 @@ def _on(stream):
     return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
+def _ready(t, dtype, k: int) -> bool:
+    """t is usable as is: a contiguous CUDA tensor of dtype and shape [n, k] (the calls' fast
+    path, which creates no temporaries and so needs no stream context)."""
+    return (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.dim() == 2
+            and t.shape[1] == k and t.is_contiguous())
+
+
 def _hits(hits, n: int, device, name="hits"):
     """A caller-supplied record buffer must hold n float32 [4] records on `device`."""
     if hits is None:
@@ -341,6 +348,14 @@ def intersect(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: in
               hits: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """fiber_intersect: rays f32[n_rays,8], pairs i32[n_pairs,2] (CUDA) -> hits f32[n_pairs,4]
     (t, u, n_oct bits, flags bits); see unpack()."""
+    if (hits is not None and _ready(rays, torch.float32, 8) and _ready(pairs, torch.int32, 2)
+            and _ready(hits, torch.float32, 4) and hits.shape[0] >= pairs.shape[0]
+            and rays.get_device() == pairs.get_device() == hits.get_device()):
+        # fast path (a pipelined caller's per-launch call): nothing to convert or allocate
+        _check(lib().fiber_intersect(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
+                                     pairs.data_ptr(), pairs.shape[0], int(depth),
+                                     hits.data_ptr(), _stream(stream)), "fiber_intersect")
+        return hits
     with _on(stream):
         rays, pairs = _args(rays, pairs)
         if hits is None:
@@ -417,6 +432,18 @@ def compact_hits(hits: torch.Tensor, out: torch.Tensor | None = None,
                  with_idx: bool = True, stream=None):
     """fiber_compact_hits: (out f32[n,4], idx i32[n] or None, count i32[1]) on the device;
     out[:count] are the records with FIBER_HIT in pair order, idx[:count] their pair indices."""
+    if (out is not None and idx is not None and count is not None
+            and _ready(hits, torch.float32, 4) and _ready(out, torch.float32, 4)
+            and out.shape[0] >= hits.shape[0] and isinstance(idx, torch.Tensor)
+            and idx.dtype == torch.int32 and idx.is_contiguous() and idx.numel() >= hits.shape[0]
+            and isinstance(count, torch.Tensor) and count.dtype == torch.int32
+            and count.numel() >= 1
+            and hits.get_device() == out.get_device() == idx.get_device() == count.get_device()):
+        # fast path: caller-supplied buffers, nothing to allocate
+        _check(lib().fiber_compact_hits(hits.data_ptr(), hits.shape[0], out.data_ptr(),
+                                        idx.data_ptr(), count.data_ptr(), _stream(stream)),
+               "fiber_compact_hits")
+        return out, idx, count
     with _on(stream):
         hits = _dev(hits, torch.float32, (4,), "hits")
         n = hits.shape[0]
