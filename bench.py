@@ -229,11 +229,13 @@ def _flush_fn(dev):
 
 def time_launches(fx, data, depth_list, steps, warmup, flush, stream, hits):
     """Every (data index, depth) launch of a step, L2 flushed before each, with CUDA events
-    around the whole call and between its traversal and finalisation kernels.  Returns the
-    per-launch [steps, L] total and K2 times in ms."""
+    around the whole call (the library's own call: K3 launched as a programmatic dependent of
+    K2) -- and, in a second pass, with an event between the traversal and finalisation kernels
+    for K2's own time (an event between them turns the programmatic launch off, so it is not
+    in the totals).  Returns the per-launch [steps, L] total and K2 times in ms."""
     import torch
 
-    def one(record):
+    def one(record, split):
         evs = []
         for di, D in depth_list:
             rays, segs, pairs = data[di]
@@ -241,20 +243,25 @@ def time_launches(fx, data, depth_list, steps, warmup, flush, stream, hits):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
             if record:
                 ev[0].record(stream)
-            fx.intersect_ex(rays, segs, pairs, D, hits=hits[:pairs.shape[0]],
-                            event_after_traverse=ev[1] if record else None)
+            if split:
+                fx.intersect_ex(rays, segs, pairs, D, hits=hits[:pairs.shape[0]],
+                                event_after_traverse=ev[1] if record else None)
+            else:
+                fx.intersect(rays, segs, pairs, D, hits=hits[:pairs.shape[0]])
             if record:
                 ev[2].record(stream)
                 evs.append(ev)
         return evs
 
     for _ in range(warmup):
-        one(False)
+        one(False, False)
     torch.cuda.synchronize()
-    all_ev = [one(True) for _ in range(steps)]
+    all_ev = [one(True, False) for _ in range(steps)]
+    torch.cuda.synchronize()
+    k2_ev = [one(True, True) for _ in range(steps)]
     torch.cuda.synchronize()
     tot = np.array([[e[0].elapsed_time(e[2]) for e in s] for s in all_ev])
-    k2 = np.array([[e[0].elapsed_time(e[1]) for e in s] for s in all_ev])
+    k2 = np.array([[e[0].elapsed_time(e[1]) for e in s] for s in k2_ev])
     return tot, k2
 
 
@@ -399,9 +406,9 @@ def run_ours(args):
     wall = time.perf_counter() - t0
     total_ms = _max_over_ranks(float(step_ms.sum()), dev)
     value = world * pairs_per_step * args.steps / (total_ms * 1e-3) / 1e9
-    # the same launches serialised, the L2 flushed before each one, each bracketed by events
-    # (with one between its traversal and finalisation kernels): the per-depth curve and the
-    # K2 time of the roofline
+    # the same launches serialised, the L2 flushed before each one, each bracketed by events:
+    # the per-depth curve; and a second pass with an event between K2 and K3: K2's time for
+    # the roofline
     per_launch, per_k2 = time_launches(fx, data, launches, args.steps, 1, flush, stream, hits)
     ser_ms = _max_over_ranks(float(per_launch.sum()), dev)
 
@@ -438,7 +445,8 @@ def run_ours(args):
         "value_serialized": round(world * pairs_per_step * args.steps / (ser_ms * 1e-3) / 1e9, 4),
         "value_note": f"value: whole steps, the 63 launches issued back to back on {args.streams} streams (L2 "
                       "flushed before each step); value_serialized: the sum of the launches timed "
-                      "one by one, L2 flushed before each (by_depth and the roofline use these)",
+                      "one by one, L2 flushed before each (by_depth uses these); K2's time for the "
+                      "roofline from a second such pass with an event between K2 and K3",
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded; workloads/gen.py config2..5)",
         "config": {"workload": "C2: single cubic fiber x 2^20 random rays, fibers F_A/F_B/F_C, "
