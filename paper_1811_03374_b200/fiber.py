@@ -350,7 +350,8 @@ def intersect(rays: torch.Tensor, segs: Segments, pairs: torch.Tensor, depth: in
     (t, u, n_oct bits, flags bits); see unpack()."""
     if (hits is not None and _ready(rays, torch.float32, 8) and _ready(pairs, torch.int32, 2)
             and _ready(hits, torch.float32, 4) and hits.shape[0] >= pairs.shape[0]
-            and rays.get_device() == pairs.get_device() == hits.get_device()):
+            and rays.get_device() == pairs.get_device() == hits.get_device()
+            == torch.cuda.current_device()):
         # fast path (a pipelined caller's per-launch call): nothing to convert or allocate
         _check(lib().fiber_intersect(rays.data_ptr(), rays.shape[0], ctypes.byref(segs.desc),
                                      pairs.data_ptr(), pairs.shape[0], int(depth),
@@ -438,7 +439,8 @@ def compact_hits(hits: torch.Tensor, out: torch.Tensor | None = None,
             and idx.dtype == torch.int32 and idx.is_contiguous() and idx.numel() >= hits.shape[0]
             and isinstance(count, torch.Tensor) and count.dtype == torch.int32
             and count.numel() >= 1
-            and hits.get_device() == out.get_device() == idx.get_device() == count.get_device()):
+            and hits.get_device() == out.get_device() == idx.get_device() == count.get_device()
+            == torch.cuda.current_device()):
         # fast path: caller-supplied buffers, nothing to allocate
         _check(lib().fiber_compact_hits(hits.data_ptr(), hits.shape[0], out.data_ptr(),
                                         idx.data_ptr(), count.data_ptr(), _stream(stream)),
