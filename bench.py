@@ -65,6 +65,7 @@ N_RAYS = 1 << 20
 #   a7 FP32 finalisation of a hit (frame back-rotation, u, normal, octahedral encoding)  69
 FLOPS_SETUP, FLOPS_TEST, FLOPS_DESCEND, FLOPS_BACKTRACK, FLOPS_FIN = 189, 82, 57, 57, 69
 PROFILE = "profiles/r2_ncu_K2_fiberA_D22.txt"  # ncu --set full summary, stamped with the .so hash
+PROFILES_CFG = {"C3": "profiles/r2_ncu_K2_C3.txt", "C4": "profiles/r2_ncu_K2_C4.txt"}  # the same
 
 
 def parse():
@@ -190,12 +191,12 @@ def fp32_peak_tflops(sms: int, mhz: float) -> float:
     return sms * 128 * 2 * mhz * 1e6 / 1e12
 
 
-def profile_metrics(sha: str) -> dict:
-    """K2's metrics in the committed ncu summary, only if it was taken of this build."""
-    path = os.path.join(ROOT, PROFILE)
+def profile_metrics(sha: str, rel: str = PROFILE) -> dict:
+    """K2's metrics in a committed ncu summary, only if it was taken of this build."""
+    path = os.path.join(ROOT, rel)
     out, in_k2, stamp = {}, False, None
     if not os.path.exists(path):
-        return {"profile": PROFILE, "profile_matches_build": False}
+        return {"profile": rel, "profile_matches_build": False}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for line in open(path):
         if line.startswith("# libfiber.so build stamp:"):
@@ -208,7 +209,7 @@ def profile_metrics(sha: str) -> dict:
                 out[parts[0]] = float(parts[1]) * (scale.get(parts[2], 1) if len(parts) > 2 else 1)
             except ValueError:
                 pass
-    res = {"profile": PROFILE, "profile_matches_build": stamp == sha, "profile_sha256": stamp}
+    res = {"profile": rel, "profile_matches_build": stamp == sha, "profile_sha256": stamp}
     if stamp != sha:
         return res
     issue = out.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
@@ -468,7 +469,7 @@ def run_ours(args):
     }
     samples = {}
     if world == 1 and not args.no_configs:
-        out["configs"], samples = run_configs(args, fx, dev, flush, stream, peak, prof)
+        out["configs"], samples = run_configs(args, fx, dev, flush, stream, peak, sha)
         out["gpu_launches"] += sum(2 * args.steps for _ in out["configs"])
     if not args.no_c5:
         out["c5"], c5_sample = run_c5(args, fx, dev, world, rank, peak)
@@ -485,7 +486,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_configs(args, fx, dev, flush, stream, peak, prof):
+def run_configs(args, fx, dev, flush, stream, peak, sha):
     """BASELINE configs 3 and 4 at full size (N = 1): device-timed like the C2 launches."""
     import torch
 
@@ -512,7 +513,8 @@ def run_configs(args, fx, dev, flush, stream, peak, prof):
                      "k3_share": round(1 - ms_k2 / ms, 3),
                      "hit_fraction": round(hitf, 4),
                      "tests_per_pair": round(tests_pp, 3),
-                     "roofline": roofline(flops, ms_k2, peak, {}, w.n_pairs, bpp),
+                     "roofline": roofline(flops, ms_k2, peak,
+                                          profile_metrics(sha, PROFILES_CFG[name]), w.n_pairs, bpp),
                      "gen_s": round(t_gen, 1)}
         rng = np.random.default_rng(17)
         sub = np.sort(rng.choice(w.n_pairs, 2048, replace=False))
