@@ -468,6 +468,8 @@ def run_ours(args):
         "libfiber_build_stamp": sha,
     }
     samples = {}
+    if not args.no_e2e:  # right after the C2 steps it is measured against, before C3-C5
+        out["e2e"] = e2e(args, fx, wls, dev, depths)
     if world == 1 and not args.no_configs:
         out["configs"], samples = run_configs(args, fx, dev, flush, stream, peak, sha)
         out["gpu_launches"] += sum(2 * args.steps for _ in out["configs"])
@@ -476,8 +478,6 @@ def run_ours(args):
         out["gpu_launches"] += out["c5"].pop("_launches")
         if c5_sample is not None:
             samples["C5"] = c5_sample
-    if not args.no_e2e:
-        out["e2e"] = e2e(args, fx, wls, dev, depths)
     if rank == 0 and not args.no_cpu and world == 1:
         out["cpu_baseline"] = cpu_baseline(samples)
     if rank == 0:
