@@ -594,11 +594,13 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
     host: its hit records in pair order (fiber_compact_hits: the records with FIBER_HIT and
     their pair indices; a pair without a hit carries no result) and their count.
     Pipelined as an application would: copies run on their own streams and overlap the
-    launches, and the 63 independent launches alternate between two compute streams (the
+    launches; the 63 independent launches alternate between three compute streams (the
     library is stream-safe), so one launch's latency-bound FP64 tail (K3) overlaps the next
-    launch's traversal.  The next fiber's inputs upload while this fiber's depths run; launch
-    i's hits download while later launches compute (a ring of R result slots; the host reads
-    launch i's count L launches behind the compute it enqueues)."""
+    launch's traversal.  The inputs are double-buffered: step s+1's uploads are issued at the
+    start of step s and run under its launches (the timed region holds exactly one upload of
+    every step's inputs, the first one included); launch i's hits download while later
+    launches compute (a ring of R result slots; the host reads launch i's count L launches
+    behind the compute it enqueues)."""
     import collections
 
     import torch
@@ -611,10 +613,11 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                      torch.from_numpy(w.ctrl).pin_memory(), torch.from_numpy(w.radii).pin_memory()))
     nb = len(host)
     NC = 3  # compute streams
-    d_in = [(torch.empty((n, 8), dtype=torch.float32, device=dev),
-             torch.empty((n, 2), dtype=torch.int32, device=dev),
-             torch.empty((1, 4, 3), dtype=torch.float32, device=dev),
-             torch.empty((1, 4), dtype=torch.float32, device=dev)) for _ in range(nb)]
+    d_in = [[(torch.empty((n, 8), dtype=torch.float32, device=dev),
+              torch.empty((n, 2), dtype=torch.int32, device=dev),
+              torch.empty((1, 4, 3), dtype=torch.float32, device=dev),
+              torch.empty((1, 4), dtype=torch.float32, device=dev)) for _ in range(nb)]
+            for _ in range(2)]  # two input sets: step s uses set s % 2
     d_hits = [torch.empty((n, 4), dtype=torch.float32, device=dev) for _ in range(NC)]
     R, LAG = 8, 4
     d_out = [torch.empty((n, 4), dtype=torch.float32, device=dev) for _ in range(R)]
@@ -633,12 +636,13 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
     # they would hold the host (which reads each count before it can size that launch's
     # copy) and with it the launches it has yet to enqueue
     cnt = torch.cuda.Stream(device=dev)
-    ev_in = [torch.cuda.Event() for _ in range(nb)]
-    ev_used = [[torch.cuda.Event() for _ in range(NC)] for _ in range(nb)]  # fiber f consumed
+    ev_in = [[torch.cuda.Event() for _ in range(nb)] for _ in range(2)]
+    # set q, fiber f consumed by every compute stream (before set q is overwritten)
+    ev_used = [[[torch.cuda.Event() for _ in range(NC)] for _ in range(nb)] for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(R)]
     ev_cnt = [torch.cuda.Event() for _ in range(R)]
     ev_free = [torch.cuda.Event() for _ in range(R)]
-    for e in [x for row in ev_used for x in row] + ev_free:
+    for e in [x for q in ev_used for row in q for x in row] + ev_free:
         e.record(main)
     counts = {"h2d": 0, "d2h": 0, "hits": 0, "wait_s": 0.0}
 
@@ -655,30 +659,34 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
         counts["d2h"] += 4 + 20 * k
         counts["hits"] += k
 
-    def step():
-        counts["h2d"] = counts["d2h"] = counts["hits"] = 0
-        counts["wait_s"] = 0.0
-        for c in comps + [up, down, cnt]:
-            c.wait_stream(main)
-        with torch.cuda.stream(up):  # all uploads of the step, in order, on the copy stream
+    def upload(q):
+        """One step's inputs into set q, on the copy stream (after set q's last use)."""
+        up.wait_stream(main)
+        with torch.cuda.stream(up):
             for f, (r, p, c, ra) in enumerate(host):
-                for e in ev_used[f]:
+                for e in ev_used[q][f]:
                     up.wait_event(e)
-                for dst, src in zip(d_in[f], (r, p, c, ra)):
+                for dst, src in zip(d_in[q][f], (r, p, c, ra)):
                     dst.copy_(src, non_blocking=True)
                     counts["h2d"] += src.numel() * 4
-                ev_in[f].record(up)
+                ev_in[q][f].record(up)
+
+    def step(q, prefetch):
+        for c in comps + [down, cnt]:
+            c.wait_stream(main)
+        if prefetch:  # the next step's inputs, under this step's launches
+            upload(1 - q)
         pending = collections.deque()
         keep = []  # every Segments of the step stays alive until the step is over
         j = 0
         for f in range(nb):
-            d_rays, d_pairs, d_ctrl, d_rad = d_in[f]
+            d_rays, d_pairs, d_ctrl, d_rad = d_in[q][f]
             segs, ev_seg, ready = None, torch.cuda.Event(), set()
             for D in depths:
                 s, c = j % R, j % NC
                 cs = comps[c]
                 if c not in ready:  # once per fiber and stream: its inputs and segments
-                    cs.wait_event(ev_in[f])
+                    cs.wait_event(ev_in[q][f])
                     if segs is not None:
                         cs.wait_event(ev_seg)
                     ready.add(c)
@@ -699,29 +707,38 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                 if len(pending) > LAG:
                     drain(pending.popleft())
                 j += 1
-            for c, e in zip(comps, ev_used[f]):
+            for c, e in zip(comps, ev_used[q][f]):
                 e.record(c)
         while pending:
             drain(pending.popleft())
         for c in comps + [down, cnt]:  # the step ends when its last hits are on the host
             main.wait_stream(c)
-        return counts["h2d"], counts["d2h"]
 
-    for _ in range(2):
-        step()
+    def run(k):
+        """k steps, each uploading its own inputs (the first before its launches, the others
+        during the step before) -> host seconds, host seconds waiting for counts."""
+        counts["h2d"] = counts["d2h"] = counts["hits"] = 0
+        host_s = wait_s = 0.0
+        t0 = time.perf_counter()
+        upload(0)
+        host_s += time.perf_counter() - t0
+        for s in range(k):
+            counts["wait_s"] = 0.0
+            t0 = time.perf_counter()
+            step(s % 2, s + 1 < k)
+            host_s += time.perf_counter() - t0
+            wait_s += counts["wait_s"]
+        return host_s, wait_s
+
+    run(2)
     torch.cuda.synchronize()
     if torch.distributed.is_available() and torch.distributed.is_initialized():
         torch.distributed.barrier()
         torch.cuda.synchronize()
-    k = max(1, min(args.steps, 3))
+    k = max(1, min(args.steps, 5))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
-    host_s = wait_s = 0.0
-    for _ in range(k):
-        t0 = time.perf_counter()
-        h2d, d2h = step()
-        host_s += time.perf_counter() - t0
-        wait_s += counts["wait_s"]
+    host_s, wait_s = run(k)
     e1.record(main)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -732,17 +749,17 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
         ms = _max_over_ranks(ms, dev)
     tests = world * n * len(FIBERS) * len(depths) * k
     return {"value": round(tests / (ms * 1e-3) / 1e9, 4), "unit": UNIT,
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "h2d_bytes_per_step": int(counts["h2d"] // k), "d2h_bytes_per_step": int(counts["d2h"] // k),
             "ms_per_step": round(ms / k, 3), "steps": k,
-            "hits_per_step": int(counts["hits"]),
-            # host time in step() (enqueueing + waiting for counts) and the part spent waiting:
-            # a small wait share means the host's enqueueing, not the device, sets the pace
+            "hits_per_step": int(counts["hits"] // k),
+            # host time in the steps (enqueueing + waiting for counts) and the part spent
+            # waiting: a small wait share means the host's enqueueing sets the pace
             "host_ms_per_step": round(host_s * 1e3 / k, 3),
             "host_wait_ms_per_step": round(wait_s * 1e3 / k, 3),
             "note": "results = per launch the hit records in pair order + their pair indices "
                     "(fiber_compact_hits) + the count; launches alternate between 3 compute "
-                    "streams, copies on two copy streams overlapping them (ring of 8 result slots)"}
-
+                    "streams, copies on two copy streams overlapping them (ring of 8 result "
+                    "slots); inputs double-buffered, step s+1's uploads during step s"}
 
 
 # ------------------------------------------------------------------------------- oracle
