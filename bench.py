@@ -671,13 +671,12 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                     counts["h2d"] += src.numel() * 4
                 ev_in[q][f].record(up)
 
-    def step(q, prefetch):
-        for c in comps + [down, cnt]:
-            c.wait_stream(main)
+    def step(q, prefetch, pending, keep):
+        """One step's 63 launches on input set q.  Steps follow one another without a join:
+        the slots' and the input sets' events order them, and the host keeps draining launch
+        results LAG launches behind across the step boundary."""
         if prefetch:  # the next step's inputs, under this step's launches
             upload(1 - q)
-        pending = collections.deque()
-        keep = []  # every Segments of the step stays alive until the step is over
         j = 0
         for f in range(nb):
             d_rays, d_pairs, d_ctrl, d_rad = d_in[q][f]
@@ -709,26 +708,25 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
                 j += 1
             for c, e in zip(comps, ev_used[q][f]):
                 e.record(c)
-        while pending:
-            drain(pending.popleft())
-        for c in comps + [down, cnt]:  # the step ends when its last hits are on the host
-            main.wait_stream(c)
 
     def run(k):
         """k steps, each uploading its own inputs (the first before its launches, the others
         during the step before) -> host seconds, host seconds waiting for counts."""
         counts["h2d"] = counts["d2h"] = counts["hits"] = 0
-        host_s = wait_s = 0.0
+        counts["wait_s"] = 0.0
         t0 = time.perf_counter()
+        for c in comps + [down, cnt]:
+            c.wait_stream(main)
         upload(0)
-        host_s += time.perf_counter() - t0
+        pending = collections.deque()
+        keep = []  # every Segments stays alive until the last launch is done
         for s in range(k):
-            counts["wait_s"] = 0.0
-            t0 = time.perf_counter()
-            step(s % 2, s + 1 < k)
-            host_s += time.perf_counter() - t0
-            wait_s += counts["wait_s"]
-        return host_s, wait_s
+            step(s % 2, s + 1 < k, pending, keep)
+        while pending:
+            drain(pending.popleft())
+        for c in comps + [down, cnt]:  # the run ends when the last hits are on the host
+            main.wait_stream(c)
+        return time.perf_counter() - t0, counts["wait_s"]
 
     run(2)
     torch.cuda.synchronize()
@@ -759,7 +757,7 @@ def e2e(args, fx, wls, dev, depths=DEPTHS):
             "note": "results = per launch the hit records in pair order + their pair indices "
                     "(fiber_compact_hits) + the count; launches alternate between 3 compute "
                     "streams, copies on two copy streams overlapping them (ring of 8 result "
-                    "slots); inputs double-buffered, step s+1's uploads during step s"}
+                    "slots); inputs double-buffered, step s+1's uploads during step s; steps not joined (the last hits of the run are on the host when it ends)"}
 
 
 # ------------------------------------------------------------------------------- oracle
