@@ -50,7 +50,7 @@ def gather_records(local: torch.Tensor) -> torch.Tensor:
 
 
 def nearest_keys_host(t: np.ndarray, hit: np.ndarray, pairs: np.ndarray, n_rays: int) -> np.ndarray:
-    """Host mirror of the K3 epilogue: per ray min((bits(t) << 32) | pair index), -1 = none.
+    """Host mirror of the nearest epilogue (K4): per ray min((bits(t) << 32) | pair index), -1 = none.
     (Used to check sharding logic on CPU; the GPU computes it with atomicMin.)"""
     keys = np.full(n_rays, -1, dtype=np.int64)
     idx = np.flatnonzero(hit)
@@ -114,7 +114,7 @@ def chunk_by_ray(pairs: np.ndarray, owned: np.ndarray, n_rays: int, n_chunks: in
 
 class ShardedNearest:
     """The multi-GPU path of SURVEY 8(e): this rank's ray shard, its pairs in K chunk launches of
-    fiber_intersect_nearest (K2 + the per-ray nearest epilogue) on a compute stream, and per
+    fiber_intersect_nearest (K2, K3 and the per-ray nearest pass K4) on a compute stream, and per
     chunk -- as soon as its launch is done, on a second stream -- its per-ray records
     (fiber_nearest_records) gathered from every rank with one all_gather_into_tensor, so chunk k's
     exchange overlaps chunk k+1's kernels.  No other data crosses ranks: segments are
