@@ -2,9 +2,10 @@
 //
 // A renderer consumes only the pairs that hit (the query returns the nearest
 // intersection "or nothing"), so the records worth moving off the device are the hits.  Two
-// passes over the records with the three-phase scan of scan.cuh: per-tile hit counts, a
-// scan of the tile counts, then each tile writes its hits at their global rank.  The result
-// is deterministic: out[k] is the record of the k-th hit pair in pair order.
+// passes over the records: per-tile hit counts, then each tile writes its hits at their
+// global rank -- its offset summed from the counts before it (up to 4M records), else from a
+// scan of the tile counts (scan.cuh) in between.  The result is deterministic: out[k] is the
+// record of the k-th hit pair in pair order.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -69,6 +70,35 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const uint4* __restri
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = sums[tiles];
 }
 
+// Short inputs (up to kInlineTiles tiles, 4M records): the scatter forms its tile's offset
+// itself -- a block reduction over the counts of the tiles before it (at most 16 KB, from L2)
+// -- so the compaction is two kernels and no single-block scan between them.
+constexpr int64_t kInlineTiles = 4096;
+__global__ void __launch_bounds__(kThreads) scatter_inline_kernel(const uint4* __restrict__ hits,
+                                                                 int64_t n,
+                                                                 const uint32_t* __restrict__ sums,
+                                                                 int64_t tiles,
+                                                                 uint4* __restrict__ out,
+                                                                 uint32_t* __restrict__ idx,
+                                                                 uint32_t* __restrict__ count) {
+  uint32_t part = 0, before;
+  for (uint32_t t = threadIdx.x; t < blockIdx.x; t += kThreads) part += sums[t];
+  fiberscan::block_excl(part, &before);
+  const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kPer;
+  uint32_t mask;
+  uint32_t total;
+  uint32_t run = fiberscan::block_excl(tile_hits(hits, n, base, mask), &total) + before;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if (mask & (1u << k)) {
+      out[run] = __ldg(&hits[base + k]);
+      if (idx) idx[run] = (uint32_t)(base + k);
+      ++run;
+    }
+  }
+  if (blockIdx.x == tiles - 1 && threadIdx.x == 0) *count = before + total;
+}
+
 }  // namespace fibercompact
 
 extern "C" int fiber_compact_hits(const fiber_hit* hits, int64_t n, fiber_hit* out, uint32_t* idx,
@@ -97,9 +127,14 @@ extern "C" int fiber_compact_hits(const fiber_hit* hits, int64_t n, fiber_hit* o
   }
   fibercompact::count_kernel<<<(unsigned)tiles, fibercompact::kThreads, 0, st>>>(
       (const uint4*)hits, n, sums, tiles);
-  fiberscan::scan_sums<<<1, 1024, 0, st>>>(sums, tiles + 1);
-  fibercompact::scatter_kernel<<<(unsigned)tiles, fibercompact::kThreads, 0, st>>>(
-      (const uint4*)hits, n, sums, tiles, (uint4*)out, idx, count);
+  if (tiles <= fibercompact::kInlineTiles) {
+    fibercompact::scatter_inline_kernel<<<(unsigned)tiles, fibercompact::kThreads, 0, st>>>(
+        (const uint4*)hits, n, sums, tiles, (uint4*)out, idx, count);
+  } else {
+    fiberscan::scan_sums<<<1, 1024, 0, st>>>(sums, tiles + 1);
+    fibercompact::scatter_kernel<<<(unsigned)tiles, fibercompact::kThreads, 0, st>>>(
+        (const uint4*)hits, n, sums, tiles, (uint4*)out, idx, count);
+  }
   rc = check_launch("fiber_compact_hits");
   cudaFreeAsync(sums, st);
   return rc;

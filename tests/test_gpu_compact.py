@@ -34,7 +34,7 @@ def _check(fx, hits):
     return k
 
 
-@pytest.mark.parametrize("n", [1, 31, 1023, 1024, 1025, 4097, 100_003])
+@pytest.mark.parametrize("n", [1, 31, 1023, 1024, 1025, 4097, 100_003, 4_194_304, 4_194_305])
 def test_compact_synthetic_flags_ragged_sizes(fx, n):
     """Random flag words around the tile size (1024 records) and a ragged tail."""
     import torch
