@@ -578,7 +578,8 @@ def run_c5(args, fx, dev, world, rank, peak):
            "records_bytes_gathered": int(16 * n_rays) if world > 1 else 0,
            "hit_fraction": round(hitf, 4),
            "roofline": roofline(flops, float(np.median(kern)), peak, {}, pairs.shape[0], 26.4),
-           "gen_s": round(t_gen, 1), "_launches": args.steps * (2 * K + 1)}
+           # per step: nearest_init + per chunk K2, K3, K4 (nearest keys) and the records kernel
+           "gen_s": round(t_gen, 1), "_launches": args.steps * (4 * K + 1)}
     sample = None
     if rank == 0 and world == 1:
         rng = np.random.default_rng(19)
