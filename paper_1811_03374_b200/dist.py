@@ -132,8 +132,12 @@ class ShardedNearest:
         self.blocks = [torch.from_numpy(np.asarray(b, dtype=np.int64)).to(device) for b in blocks]
         self.out = [torch.empty((self.world * len(b), 4), dtype=torch.float32, device=device)
                     for b in blocks]
-        self.compute = torch.cuda.Stream(device=device)
+        # chunks alternate between two compute streams (they touch disjoint rays), so one
+        # chunk's drain and finalisation overlap the next chunk's traversal
+        self.computes = [torch.cuda.Stream(device=device) for _ in range(2)]
+        self.compute = self.computes[0]
         self.comm = torch.cuda.Stream(device=device)
+        self.init_done = torch.cuda.Event()
         self.done = [torch.cuda.Event() for _ in blocks]
         self.nccl = self.world > 1 and dist.get_backend() == "nccl"
 
@@ -141,19 +145,24 @@ class ShardedNearest:
         """One pass over this rank's pairs.  events = (start, kernels_done, all_done) timing
         events: start and kernels_done on the compute stream, all_done on the comm stream."""
         cur = torch.cuda.current_stream()
-        self.compute.wait_stream(cur)
+        for c in self.computes:
+            c.wait_stream(cur)
         self.comm.wait_stream(cur)
         with torch.cuda.stream(self.compute):
             if events:
                 events[0].record(self.compute)
             self.fx.nearest_init(self.nearest, stream=self.compute)
-            for k in range(len(self.blocks)):
-                a, b = self.bounds[k], self.bounds[k + 1]
-                self.fx.intersect_nearest(self.rays, self.segs, self.pairs[a:b], self.depth,
-                                          self.nearest, hits=self.hits[a:b], stream=self.compute)
-                self.done[k].record(self.compute)
-            if events:
-                events[1].record(self.compute)
+            self.init_done.record(self.compute)
+        self.computes[1].wait_event(self.init_done)
+        for k in range(len(self.blocks)):
+            cs = self.computes[k % 2]
+            a, b = self.bounds[k], self.bounds[k + 1]
+            self.fx.intersect_nearest(self.rays, self.segs, self.pairs[a:b], self.depth,
+                                      self.nearest, hits=self.hits[a:b], stream=cs)
+            self.done[k].record(cs)
+        self.compute.wait_stream(self.computes[1])
+        if events:
+            events[1].record(self.compute)
         with torch.cuda.stream(self.comm):
             for k in range(len(self.blocks)):
                 a, b = self.bounds[k], self.bounds[k + 1]
@@ -168,7 +177,8 @@ class ShardedNearest:
                     self.out[k].copy_(rec)
             if events:
                 events[2].record(self.comm)
-        cur.wait_stream(self.compute)
+        for c in self.computes:
+            cur.wait_stream(c)
         cur.wait_stream(self.comm)
 
     def records_by_ray(self, n_rays: int, all_owned) -> torch.Tensor:
